@@ -1,0 +1,26 @@
+"""B200-native (sm_100a) Localized Topological Simplification hot path.
+
+Drop-in for the reference's LTS path (arXiv 2009.00083): the Python argument
+surface of SPEC's engine (simplify_field / remove_extrema) and the reference's
+order.py / critical.py / triangulation.py types, backed by hand-written CUDA in
+liblts_sm100.so.  See DESIGN.md.
+"""
+from .errors import (ConstraintNotExtremum, FieldError, LocalizeError, LTSNativeError, MeshError,
+                     NoSaddleError, VerifyError)
+from .triangulation import Triangulation, build_grid_triangulation, grid_link_tables, link_adjacency
+from .order import (OrderField, ScalarField, ZetaMode, ZetaPolicy, compute_order_field,
+                    order_from_ranks)
+from .critical import (CriticalSet, Criticality, Kind, classify_all, classify_vertex,
+                       extract_critical_points, extrema)
+from .engine import (ConstraintSet, PassRegions, SimplifyOptions, SimplifyReport, discover_regions,
+                     remove_extrema, remove_pass, simplify_field, simplify_raw, verify_constraints)
+
+__all__ = [
+    "ConstraintNotExtremum", "FieldError", "LocalizeError", "LTSNativeError", "MeshError",
+    "NoSaddleError", "VerifyError", "Triangulation", "build_grid_triangulation", "grid_link_tables",
+    "link_adjacency", "OrderField", "ScalarField", "ZetaMode", "ZetaPolicy", "compute_order_field",
+    "order_from_ranks", "CriticalSet", "Criticality", "Kind", "classify_all", "classify_vertex",
+    "extract_critical_points", "extrema", "ConstraintSet", "PassRegions", "SimplifyOptions",
+    "SimplifyReport", "discover_regions", "remove_extrema", "remove_pass", "simplify_field",
+    "simplify_raw", "verify_constraints",
+]

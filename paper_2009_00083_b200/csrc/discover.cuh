@@ -1,0 +1,349 @@
+// discover.cuh -- region discovery (reference discover_sweep, _kernels.py:194-303)
+// as a schedule-free data-parallel computation.
+//
+// The reference sweeps one global max-heap; its result is characterised
+// exactly: v is CLAIMED iff the component of
+// {u : rank u >= rank v} that contains v has all its maxima in the seed set D;
+// regions are the connected components of claimed vertices; a region's saddle
+// is its highest unclaimed neighbour; topseed is its highest rank.
+//
+// B200 formulation (no priority queue, no sequential sweep):
+//  1. steepest-ascent forest (fused into classification) compressed to the
+//     ascending-manifold maximum M(v) of every vertex;
+//  2. cross-manifold edges (a=M(u), b=M(v), w=min(rank u, rank v)) form the
+//     maxima graph; the join-tree connectivity of superlevel sets equals its
+//     connectivity through edges of weight >= t;
+//  3. tau(m) = bottleneck from maximum m to a preserved maximum, computed by
+//     Boruvka rounds: every non-preserved component hooks along its heaviest
+//     edge; chains reaching preserved territory are final (tau = edge weight,
+//     non-decreasing along the chain), chains ending in 2-cycles contract;
+//  4. claimed(v) <=> M(v) in D and rank v > tau(M(v)); saddle = vertex of
+//     rank tau; regions = union-find over edges between claimed endpoints.
+// Parity with the reference sweep is checked in tests/test_gpu_parity.py.
+#pragma once
+#include "lts_common.cuh"
+
+namespace lts {
+
+extern int64_t g_launches;
+
+// root of a pointer forest by path halving; concurrent callers only ever
+// write ancestors, so races are benign
+__device__ __forceinline__ int forest_root(int *p, int x) {
+  for (;;) {
+    int q = ((volatile int *)p)[x];
+    if (q == x) return x;
+    int r = ((volatile int *)p)[q];
+    if (r != q) p[x] = r;
+    x = q;
+  }
+}
+
+__global__ void k_compress(int *ptr, int64_t n) {
+  GRID_STRIDE(v, n) {
+    int r = forest_root(ptr, (int)v);
+    ptr[v] = r;
+  }
+}
+
+// vertex class: 1 = discarded maximum (seed, in D), 2 = preserved maximum (P)
+__global__ void k_mark_maxima(const uint8_t *__restrict__ flags, const uint8_t *__restrict__ pmark,
+                              int kind, int64_t n, uint8_t *vcls, uint8_t *cst, int *mlist,
+                              int *counts /* [0]=maxima [1]=D [2]=P */, int *comp, int *par,
+                              int *acc, int *rpar) {
+  GRID_STRIDE(v, n) {
+    uint8_t fl = flags[v];
+    bool ext = kind == 0 ? (fl & FL_MAX) : (fl & FL_MIN);
+    bool pres = kind == 0 ? (pmark[v] & PM_MAX) : (pmark[v] & PM_MIN);
+    uint8_t c = ext ? (pres ? 2 : 1) : 0;
+    vcls[v] = c;
+    unsigned act = __activemask();
+    unsigned md = __ballot_sync(act, c == 1);
+    unsigned mp = __ballot_sync(act, c == 2);
+    unsigned mm = md | mp;
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(act) - 1;
+    int base = 0;
+    if (lane == leader && mm) {
+      base = atomicAdd(counts, __popc(mm));
+      atomicAdd(counts + 1, __popc(md));
+      atomicAdd(counts + 2, __popc(mp));
+    }
+    base = __shfl_sync(act, base, leader);
+    if (c) {
+      mlist[base + __popc(mm & lanemask_lt())] = (int)v;
+      cst[v] = c == 2 ? 1 : 0;
+      comp[v] = (int)v;
+      par[v] = (int)v;
+      acc[v] = 0x7fffffff;
+      rpar[v] = (int)v;
+    }
+  }
+}
+
+// cross-manifold edges, each grid edge once (positive offsets are the first
+// K/2 entries of the reference offset table)
+template <int NDIM>
+__global__ void k_edges(Grid g, const int *__restrict__ rank, int rev, const int *__restrict__ M,
+                        const uint8_t *__restrict__ vcls, int *ea, int *eb, int *ew, int *ecount) {
+  constexpr int KH = NDIM == 2 ? 3 : 7;
+  const int n = (int)g.n;
+  for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += gridDim.x * blockDim.x) {
+    int v = v0 + threadIdx.x;
+    bool in = v < n;
+    int x = 0, y = 0, z = 0, a = 0, rv = 0;
+    bool pa = false;
+    if (in) {
+      coords(g, v, x, y, z);
+      a = M[v];
+      rv = eff_rank(rank, v, rev, n);
+      pa = vcls[a] == 2;
+    }
+#pragma unroll
+    for (int k = 0; k < KH; k++) {
+      int u = in ? nbr_at(g, x, y, z, k) : -1;
+      int b = -1, w = 0;
+      bool emit = false;
+      if (u >= 0) {
+        b = M[u];
+        if (b != a && !(pa && vcls[b] == 2)) {
+          int ru = eff_rank(rank, u, rev, n);
+          w = ru < rv ? ru : rv;
+          emit = true;
+        }
+      }
+      unsigned m = __ballot_sync(0xffffffffu, emit);
+      if (m) {
+        int lane = threadIdx.x & 31;
+        int leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(ecount, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (emit) {
+          int slot = base + __popc(m & lanemask_lt());
+          ea[slot] = a;
+          eb[slot] = b;
+          ew[slot] = w;
+        }
+      }
+    }
+  }
+}
+
+// ---- Boruvka rounds over the maxima graph --------------------------------
+
+__device__ __forceinline__ unsigned long long bv_pack(int w, int c) {
+  return ((unsigned long long)(unsigned)(w + 1) << 32) | (unsigned)c;
+}
+
+__global__ void k_bv_reset(const int *__restrict__ mlist, int nm, unsigned long long *best) {
+  GRID_STRIDE(i, nm) best[mlist[i]] = 0ull;
+}
+
+__global__ void k_bv_best(const int *__restrict__ ea, const int *__restrict__ eb,
+                          const int *__restrict__ ew, int ne, const int *__restrict__ comp,
+                          const uint8_t *__restrict__ cst, unsigned long long *best) {
+  GRID_STRIDE(i, ne) {
+    int ca = comp[ea[i]], cb = comp[eb[i]];
+    if (ca == cb) continue;
+    int w = ew[i];
+    if (cst[ca] == 0) atomicMax(best + ca, bv_pack(w, cb));
+    if (cst[cb] == 0) atomicMax(best + cb, bv_pack(w, ca));
+  }
+}
+
+// active root: comp[m] == m && cst[m] == 0
+__global__ void k_bv_hook(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
+                          const uint8_t *__restrict__ cst, const unsigned long long *__restrict__ best,
+                          int *par, int *wc, int *err) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    if (comp[m] != m || cst[m] != 0) continue;
+    unsigned long long b = best[m];
+    if (b == 0ull) {  // isolated pure component: no preserved maximum reachable
+      atomicOr(err, 1);
+      par[m] = m;
+      wc[m] = -1;
+      continue;
+    }
+    par[m] = (int)(unsigned)(b & 0xffffffffull);
+    wc[m] = (int)(b >> 32) - 1;
+  }
+}
+
+__global__ void k_bv_cycle(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
+                           const uint8_t *__restrict__ cst, int *par) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    if (comp[m] != m || cst[m] != 0) continue;
+    int q = par[m];
+    if (q != m && cst[q] == 0 && comp[q] == q && par[q] == m && m < q) par[m] = m;
+  }
+}
+
+__global__ void k_bv_jump(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
+                          const uint8_t *__restrict__ cst, int *par) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    if (comp[m] != m || cst[m] != 0) continue;
+    par[m] = forest_root(par, m);
+  }
+}
+
+// members: tau accumulator and new component; comp is read through a snapshot
+// of the round's roots (par of the old root), so the update order is irrelevant
+__global__ void k_bv_members(const int *__restrict__ mlist, int nm, int *comp,
+                             const uint8_t *__restrict__ cst, const int *__restrict__ par,
+                             const int *__restrict__ wc, int *acc) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    int c = comp[m];
+    if (cst[c] != 0) continue;  // preserved or already final
+    int w = wc[c];
+    if (w < acc[m]) acc[m] = w;
+    comp[m] = par[c];  // root was written by k_bv_jump (par of a root is its root)
+  }
+}
+
+// after members moved: roots that reached preserved territory become final;
+// count remaining active roots (2-cycle roots)
+__global__ void k_bv_settle(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
+                            uint8_t *cst, int *active) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    if (cst[m] != 0) continue;
+    int c = comp[m];
+    if (c != m) {
+      // m is no longer a root; its component state follows its root
+      if (cst[c] != 0) cst[m] = 1;
+      continue;
+    }
+    atomicAdd(active, 1);
+  }
+}
+
+// ---- claimed set and regions -----------------------------------------------
+
+__device__ __forceinline__ int uf_find(int *p, int x) { return forest_root(p, x); }
+
+__device__ __forceinline__ void uf_union(int *p, int a, int b) {
+  for (;;) {
+    a = uf_find(p, a);
+    b = uf_find(p, b);
+    if (a == b) return;
+    if (a > b) {
+      int t = a;
+      a = b;
+      b = t;
+    }
+    // hook the larger root under the smaller
+    if (atomicCAS(p + b, b, a) == b) return;
+  }
+}
+
+__global__ void k_region_union(const int *__restrict__ ea, const int *__restrict__ eb,
+                               const int *__restrict__ ew, int ne, const uint8_t *__restrict__ vcls,
+                               const int *__restrict__ acc, int *rpar) {
+  GRID_STRIDE(i, ne) {
+    int a = ea[i], b = eb[i];
+    if (vcls[a] != 1 || vcls[b] != 1) continue;
+    if (ew[i] <= acc[a]) continue;  // an endpoint at or below the saddle level
+    uf_union(rpar, a, b);
+  }
+}
+
+__global__ void k_region_roots(const int *__restrict__ mlist, int nm, const uint8_t *__restrict__ vcls,
+                               const int *__restrict__ acc, const int *__restrict__ rank, int rev,
+                               int n, int *rpar, int *ridx, int *nreg, int *rsad, int *rtop,
+                               int *rsize) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    if (vcls[m] != 1) continue;
+    int r = uf_find(rpar, m);
+    if (r == m) {
+      int id = atomicAdd(nreg, 1);
+      ridx[m] = id;
+      rsad[id] = acc[m];  // saddle rank (effective order)
+      rtop[id] = -1;
+      rsize[id] = 0;
+    }
+  }
+}
+
+__global__ void k_region_tops(const int *__restrict__ mlist, int nm, const uint8_t *__restrict__ vcls,
+                              const int *__restrict__ rank, int rev, int n, int *rpar,
+                              const int *__restrict__ ridx, int *rtop) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    if (vcls[m] != 1) continue;
+    int r = uf_find(rpar, m);
+    atomicMax(rtop + ridx[r], eff_rank(rank, m, rev, n));
+  }
+}
+
+// claimed <=> M(v) is a seed and rank v > tau(M(v)); label and count
+__global__ void k_region_label(const int *__restrict__ rank, int rev, int n,
+                               const int *__restrict__ M, const uint8_t *__restrict__ vcls,
+                               const int *__restrict__ acc, int *rpar, const int *__restrict__ ridx,
+                               int *reg_of, int *rsize) {
+  GRID_STRIDE(v, n) {
+    int m = M[v];
+    int rid = -1;
+    if (vcls[m] == 1 && eff_rank(rank, (int)v, rev, n) > acc[m]) rid = ridx[uf_find(rpar, m)];
+    reg_of[v] = rid;
+    unsigned act = __activemask();
+    unsigned peers = __match_any_sync(act, rid);
+    if (rid >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(rsize + rid, __popc(peers));
+  }
+}
+
+// flag[t] = 1 if the vertex of effective rank t is claimed (for rank-ordered
+// compaction)
+__global__ void k_claimed_flags(const int *__restrict__ inv, int rev, int n,
+                                const int *__restrict__ reg_of, int *flag) {
+  GRID_STRIDE(t, n) {
+    int v = inv[rev ? (n - 1 - t) : t];
+    flag[t] = reg_of[v] >= 0 ? 1 : 0;
+  }
+}
+
+__global__ void k_claimed_compact(const int *__restrict__ inv, int rev, int n,
+                                  const int *__restrict__ reg_of, const int *__restrict__ pos,
+                                  uint32_t *ckey, uint32_t *cval) {
+  GRID_STRIDE(t, n) {
+    int v = inv[rev ? (n - 1 - t) : t];
+    int rid = reg_of[v];
+    if (rid >= 0) {
+      int p = pos[t];
+      ckey[p] = (uint32_t)rid;
+      cval[p] = (uint32_t)v;
+    }
+  }
+}
+
+// region sizes (+1 for the saddle) -> scan input
+__global__ void k_region_slots(const int *__restrict__ rsize, int R, int *tmp) {
+  GRID_STRIDE(i, R) tmp[i] = rsize[i] + 1;
+}
+
+__global__ void k_place(const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sval, int C,
+                        const int *__restrict__ rptr, int *verts, int *loc_of) {
+  GRID_STRIDE(j, C) {
+    int rid = (int)skey[j];
+    int v = (int)sval[j];
+    int slot = (int)j + rid + 1;
+    verts[slot] = v;
+    loc_of[v] = slot - rptr[rid];
+  }
+}
+
+__global__ void k_place_saddles(const int *__restrict__ inv, int rev, int n,
+                                const int *__restrict__ rsad, int R, const int *__restrict__ rptr,
+                                int *verts) {
+  GRID_STRIDE(r, R) {
+    int t = rsad[r];
+    verts[rptr[r]] = inv[rev ? (n - 1 - t) : t];
+  }
+}
+
+}  // namespace lts

@@ -1,0 +1,732 @@
+// lts_sm100.cu -- C ABI and device-resident orchestration of the LTS hot path
+// on B200 (sm_100a).  Unity build: every kernel header is included here so the
+// stencil tables live in one __constant__ bank.
+//
+// Pipeline:
+//   order field (onesweep radix sort)          reference order.py:86-91
+//   classification stencil                     critical.py:95-112
+//   repeat {maxima pass, minima pass,          _kernels.py:194-303, 578-591,
+//           restore, verify}
+//   realization by saddle-value gathers        contract D1
+// Host code only sequences launches on the caller's stream and reads back a
+// handful of scalars (counts) per pass; all arrays stay in HBM.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lts_common.cuh"
+#include "prims.cuh"
+#include "sort.cuh"
+#include "classify.cuh"
+#include "discover.cuh"
+#include "localize.cuh"
+#include "integrate.cuh"
+
+namespace lts {
+int64_t g_launches = 0;
+}
+
+using namespace lts;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+int lts_set_error(int code, const char *msg) {
+  g_err = msg;
+  return code;
+}
+
+int lts_set_cuda_error(cudaError_t e, const char *what, const char *file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+           cudaGetErrorString(e), file, line, what);
+  g_err = buf;
+  return LTS_E_CUDA;
+}
+
+#define LTS_TRY(x)          \
+  do {                      \
+    int rc_ = (x);          \
+    if (rc_ != 0) return rc_; \
+  } while (0)
+#define LTS_KCHECK() LTS_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------------------
+// stencil tables: offsets (triangulation.py:32-45) and the reference link-pair
+// table restated from _face_triple (triangulation.py:52-75), folded
+// into per-mask component-count LUTs.
+// ---------------------------------------------------------------------------
+static const int8_t H_OFF2[6][3] = {{1, 0, 0}, {0, 1, 0}, {1, 1, 0}, {-1, 0, 0}, {0, -1, 0}, {-1, -1, 0}};
+static const int8_t H_OFF3[14][3] = {{1, 0, 0},  {0, 1, 0},   {0, 0, 1},   {1, 1, 0},  {1, 0, 1},
+                                     {0, 1, 1},  {1, 1, 1},   {-1, 0, 0},  {0, -1, 0}, {0, 0, -1},
+                                     {-1, -1, 0}, {-1, 0, -1}, {0, -1, -1}, {-1, -1, -1}};
+
+__device__ uint8_t d_lut2[1 << 6];
+__device__ uint8_t d_lut3[1 << 14];
+
+static bool is01(const int *d, int nd) {
+  for (int a = 0; a < nd; a++)
+    if (d[a] != 0 && d[a] != 1) return false;
+  return true;
+}
+
+static bool face_triple(const int8_t *a, const int8_t *b, int nd) {
+  int z[3] = {0, 0, 0}, A[3], B[3];
+  for (int i = 0; i < 3; i++) {
+    A[i] = a[i];
+    B[i] = b[i];
+  }
+  const int *seq[6][3] = {{z, A, B}, {z, B, A}, {A, z, B}, {B, z, A}, {A, B, z}, {B, A, z}};
+  for (auto &s : seq) {
+    int d1[3], d2[3];
+    for (int i = 0; i < nd; i++) {
+      d1[i] = s[1][i] - s[0][i];
+      d2[i] = s[2][i] - s[1][i];
+    }
+    if (is01(d1, nd) && is01(d2, nd)) return true;
+  }
+  return false;
+}
+
+static void build_lut(int ndim, std::vector<uint8_t> &lut) {
+  int K = ndim == 2 ? 6 : 14;
+  const int8_t(*off)[3] = ndim == 2 ? H_OFF2 : H_OFF3;
+  std::vector<std::pair<int, int>> pairs;
+  for (int i = 0; i < K; i++)
+    for (int j = i + 1; j < K; j++)
+      if (face_triple(off[i], off[j], ndim)) pairs.emplace_back(i, j);
+  lut.assign(1u << K, 0);
+  for (unsigned m = 0; m < (1u << K); m++) {
+    int p[14];
+    for (int i = 0; i < K; i++) p[i] = i;
+    auto find = [&](int x) {
+      while (p[x] != x) x = p[x] = p[p[x]];
+      return x;
+    };
+    for (auto &e : pairs)
+      if ((m >> e.first & 1) && (m >> e.second & 1)) {
+        int a = find(e.first), b = find(e.second);
+        if (a != b) p[b] = a;
+      }
+    int c = 0;
+    for (int i = 0; i < K; i++)
+      if ((m >> i & 1) && find(i) == i) c++;
+    lut[m] = (uint8_t)c;
+  }
+}
+
+static bool g_tables_ready = false;
+
+static int init_tables() {
+  if (g_tables_ready) return 0;
+  std::vector<uint8_t> l2, l3;
+  build_lut(2, l2);
+  build_lut(3, l3);
+  LTS_CUDA(cudaMemcpyToSymbol(d_lut2, l2.data(), l2.size()));
+  LTS_CUDA(cudaMemcpyToSymbol(d_lut3, l3.data(), l3.size()));
+  g_tables_ready = true;
+  return 0;
+}
+
+static int g_off_ndim = 0;
+
+static int set_offsets(int ndim, cudaStream_t s) {
+  if (g_off_ndim == ndim) return 0;
+  int8_t off[3][kMaxK] = {};
+  int K = ndim == 2 ? 6 : 14;
+  for (int k = 0; k < K; k++)
+    for (int a = 0; a < 3; a++) off[a][k] = ndim == 2 ? H_OFF2[k][a] : H_OFF3[k][a];
+  LTS_CUDA(cudaMemcpyToSymbolAsync(c_off, off, sizeof(off), 0, cudaMemcpyHostToDevice, s));
+  LTS_CUDA(cudaStreamSynchronize(s));
+  g_off_ndim = ndim;
+  return 0;
+}
+
+static const uint8_t *lut_ptr(int ndim) {
+  void *p = nullptr;
+  cudaGetSymbolAddress(&p, ndim == 2 ? d_lut2 : d_lut3);
+  return (const uint8_t *)p;
+}
+
+// ---------------------------------------------------------------------------
+// workspace
+// ---------------------------------------------------------------------------
+struct WS {
+  // n-sized int32
+  int *rankA, *invA, *rankB, *invB, *ptr, *acc, *comp, *par, *wc, *rpar, *ridx, *reg_of, *loc_of,
+      *delta, *D, *flagscan, *mlist;
+  uint32_t *ckey, *cval, *skey, *sval;
+  // region-sized (n+1) int32
+  int *rsize, *rtop, *rsad, *order, *nit, *st, *rtmp, *rptr, *sib_rid, *pos_of, *lost, *okey;
+  uint32_t *oval, *okey2;
+  int64_t *rptr64;
+  unsigned long long *best;
+  uint8_t *flags, *pmark, *vcls, *cst;
+  int *ea, *eb, *ew;
+  int64_t emax;
+  // slots (2n)
+  int *verts, *buf0, *buf1, *buf2, *out;
+  unsigned long long *gheap;
+  uint8_t *sfl;
+  rs::Bufs sb;
+  int *bsum;
+  int *scal;  // 64 device scalars
+  size_t bytes;
+};
+
+enum {
+  SC_COUNTS = 0,   // 3
+  SC_ECOUNT = 4,
+  SC_ACTIVE = 5,
+  SC_ERR = 6,
+  SC_NREG = 7,
+  SC_S = 8,
+  SC_C = 9,
+  SC_NSHARED = 10,
+  SC_QUEUE = 11,
+  SC_STATS = 12,   // 4: nit max, capped, status1, largest
+  SC_VERIFY = 16,  // 4
+  SC_LOST = 20,
+  SC_BADPRES = 21,
+  SC_RESTORE = 24, // 3
+  SC_TMP = 28,
+  SC_N = 64
+};
+
+static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char * {
+    off = (off + 255) & ~(size_t)255;
+    char *p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  };
+  auto i32 = [&](int64_t cnt) { return (int *)take(sizeof(int) * (size_t)cnt); };
+  auto u32 = [&](int64_t cnt) { return (uint32_t *)take(sizeof(uint32_t) * (size_t)cnt); };
+  int64_t n1 = n + 1, s2 = 2 * n + 2;
+  int KH = ndim == 2 ? 3 : 7;
+  w->rankA = i32(n); w->invA = i32(n); w->rankB = i32(n); w->invB = i32(n);
+  w->ptr = i32(n); w->acc = i32(n); w->comp = i32(n); w->par = i32(n); w->wc = i32(n);
+  w->rpar = i32(n); w->ridx = i32(n); w->reg_of = i32(n); w->loc_of = i32(n);
+  w->delta = i32(n); w->D = i32(n); w->flagscan = i32(n); w->mlist = i32(n);
+  w->ckey = u32(n); w->cval = u32(n); w->skey = u32(n); w->sval = u32(n);
+  w->rsize = i32(n1); w->rtop = i32(n1); w->rsad = i32(n1); w->order = i32(n1); w->nit = i32(n1);
+  w->st = i32(n1); w->rtmp = i32(n1); w->rptr = i32(n1); w->sib_rid = i32(n1); w->pos_of = i32(n1);
+  w->lost = i32(n1); w->okey = i32(n1); w->oval = u32(n1); w->okey2 = u32(n1);
+  w->rptr64 = (int64_t *)take(sizeof(int64_t) * (size_t)n1);
+  w->best = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)n);
+  w->flags = (uint8_t *)take((size_t)n); w->pmark = (uint8_t *)take((size_t)n);
+  w->vcls = (uint8_t *)take((size_t)n); w->cst = (uint8_t *)take((size_t)n);
+  w->emax = (int64_t)KH * n;
+  w->ea = i32(w->emax); w->eb = i32(w->emax); w->ew = i32(w->emax);
+  w->verts = i32(s2); w->buf0 = i32(s2); w->buf1 = i32(s2); w->buf2 = i32(s2); w->out = i32(s2);
+  w->gheap = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)s2);
+  w->sfl = (uint8_t *)take((size_t)s2);
+  w->sb.k1 = u32(n); w->sb.v1 = u32(n); w->sb.k2 = u32(n); w->sb.v2 = u32(n);
+  w->sb.status = u32(rs::status_elems(n));
+  w->sb.hist = u32(4 * 256);
+  w->sb.ctr = u32(8);
+  w->sb.nonfinite = i32(4);
+  w->bsum = i32(n / SCAN_TILE + 2);
+  w->scal = i32(SC_N);
+  w->bytes = off + 256;
+  return (int64_t)w->bytes;
+}
+
+// ---------------------------------------------------------------------------
+// context, scalar readback, timing
+// ---------------------------------------------------------------------------
+struct Ctx {
+  Grid g;
+  int64_t n;
+  WS w;
+  cudaStream_t s;
+  const uint8_t *lut;
+  int *h_scal;  // pinned
+  bool timing;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+};
+
+static int *g_h_scal = nullptr;
+static std::vector<cudaEvent_t> g_events;
+static size_t g_ev_next = 0;
+
+static cudaEvent_t next_event() {
+  if (g_ev_next >= g_events.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_events.push_back(e);
+  }
+  return g_events[g_ev_next++];
+}
+
+struct Phase {
+  Ctx &c;
+  int id;
+  cudaEvent_t a;
+  Phase(Ctx &c_, int id_) : c(c_), id(id_), a(nullptr) {
+    if (c.timing) {
+      a = next_event();
+      cudaEventRecord(a, c.s);
+    }
+  }
+  ~Phase() {
+    if (c.timing) {
+      cudaEvent_t b = next_event();
+      cudaEventRecord(b, c.s);
+      c.marks.push_back({id, {a, b}});
+    }
+  }
+};
+
+static int readback(Ctx &c, int first, int count) {
+  LTS_CUDA(cudaMemcpyAsync(c.h_scal + first, c.w.scal + first, sizeof(int) * count,
+                           cudaMemcpyDeviceToHost, c.s));
+  LTS_CUDA(cudaStreamSynchronize(c.s));
+  return 0;
+}
+
+static int bits_for(int64_t maxval) {
+  int b = 1;
+  while (b < 32 && ((int64_t)1 << b) <= maxval) b++;
+  return b;
+}
+
+static int setup(Ctx &c, int ndim, const int64_t *dims, void *ws, size_t ws_bytes, void *stream) {
+  if (ndim != 2 && ndim != 3) return lts_set_error(LTS_E_BAD_DIMS, "grid must be 2D or 3D");
+  int64_t n = 1;
+  for (int a = 0; a < ndim; a++) {
+    if (dims[a] < 2) return lts_set_error(LTS_E_BAD_DIMS, "every grid axis needs at least 2 vertices");
+    n *= dims[a];
+  }
+  if (n >= (int64_t)1 << 30) return lts_set_error(LTS_E_BAD_DIMS, "grid too large (n >= 2^30)");
+  c.g.nx = (int)dims[0];
+  c.g.ny = (int)dims[1];
+  c.g.nz = ndim == 3 ? (int)dims[2] : 1;
+  c.g.ndim = ndim;
+  c.g.K = ndim == 2 ? 6 : 14;
+  c.g.n = n;
+  c.n = n;
+  c.s = (cudaStream_t)stream;
+  int64_t need = carve(&c.w, nullptr, ndim, n);
+  if (ws != nullptr) {
+    if ((size_t)need > ws_bytes) return lts_set_error(LTS_E_WORKSPACE, "workspace too small");
+    carve(&c.w, (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255), ndim, n);
+  }
+  LTS_TRY(init_tables());
+  LTS_TRY(set_offsets(ndim, c.s));
+  c.lut = lut_ptr(ndim);
+  if (!g_h_scal) LTS_CUDA(cudaHostAlloc((void **)&g_h_scal, sizeof(int) * SC_N, cudaHostAllocDefault));
+  c.h_scal = g_h_scal;
+  c.timing = false;
+  g_ev_next = 0;
+  return 0;
+}
+
+#define NB(nn) grid_blocks((nn), 256)
+
+// ---------------------------------------------------------------------------
+// one removal pass (maxima pass, or minima pass on the reversed order)
+// ---------------------------------------------------------------------------
+__global__ void k_loc_stats(const int *nit, const int *st, const int *rsize, int R, int *out) {
+  GRID_STRIDE(r, R) {
+    atomicMax(out + 0, nit[r]);
+    if (st[r] == 2) atomicAdd(out + 1, 1);
+    if (st[r] == 1) atomicAdd(out + 2, 1);
+    atomicMax(out + 3, rsize[r] + 1);
+  }
+}
+
+__global__ void k_order_keys(const int *rsize, int R, uint32_t *key) {
+  GRID_STRIDE(r, R) key[r] = 0x7fffffffu - (uint32_t)rsize[r];
+}
+
+static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uint8_t *pmark,
+                    int max_iter, int *new_rank, int *new_inv, float *g, lts_pass_report_t *rep,
+                    lts_regions_view_t *view) {
+  WS &w = c.w;
+  const int64_t n = c.n;
+  const int ni = (int)n;
+  const int rev = kind;
+  cudaStream_t s = c.s;
+  lts_pass_report_t r{};
+  r.kind = kind;
+  int R = 0, C = 0, S = 0;
+  {
+    Phase ph(c, LTS_PH_CLASSIFY);
+    launch_classify(c.g, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
+    LTS_KCHECK();
+  }
+  {
+    Phase ph(c, LTS_PH_DISCOVER);
+    LTS_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(int) * SC_N, s));
+    k_mark_maxima<<<NB(n), 256, 0, s>>>(w.flags, pmark, kind, n, w.vcls, w.cst, w.mlist,
+                                         w.scal + SC_COUNTS, w.comp, w.par, w.acc, w.rpar);
+    g_launches++;
+    LTS_KCHECK();
+    LTS_TRY(readback(c, SC_COUNTS, 3));
+    const int nm = c.h_scal[SC_COUNTS], nD = c.h_scal[SC_COUNTS + 1], nP = c.h_scal[SC_COUNTS + 2];
+    r.seeds = nD;
+    if (nD == 0) {
+      LTS_CUDA(cudaMemcpyAsync(new_rank, rank, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+      LTS_CUDA(cudaMemcpyAsync(new_inv, inv, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+      if (rep) *rep = r;
+      if (view) memset(view, 0, sizeof(*view));
+      return 0;
+    }
+    if (nP == 0) return lts_set_error(LTS_E_NO_SADDLE, "every extremum of this kind is discarded: no saddle");
+    k_compress<<<NB(n), 256, 0, s>>>(w.ptr, n);
+    if (c.g.ndim == 2)
+      k_edges<2><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.ptr, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
+    else
+      k_edges<3><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.ptr, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
+    g_launches += 2;
+    LTS_KCHECK();
+    LTS_TRY(readback(c, SC_ECOUNT, 1));
+    const int ne = c.h_scal[SC_ECOUNT];
+    // Boruvka rounds: tau(m) = bottleneck to preserved maxima
+    for (int round = 0; round < 64; round++) {
+      k_bv_reset<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.best);
+      k_bv_best<<<NB(ne), 256, 0, s>>>(w.ea, w.eb, w.ew, ne, w.comp, w.cst, w.best);
+      k_bv_hook<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.best, w.par, w.wc, w.scal + SC_ERR);
+      k_bv_cycle<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par);
+      k_bv_jump<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par);
+      k_bv_members<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par, w.wc, w.acc);
+      LTS_CUDA(cudaMemsetAsync(w.scal + SC_ACTIVE, 0, sizeof(int), s));
+      k_bv_settle<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.scal + SC_ACTIVE);
+      g_launches += 7;
+      LTS_KCHECK();
+      LTS_TRY(readback(c, SC_ACTIVE, 2));
+      if (c.h_scal[SC_ERR]) return lts_set_error(LTS_E_NO_SADDLE, "a discarded extremum cannot reach a preserved one");
+      if (c.h_scal[SC_ACTIVE] == 0) break;
+    }
+    // regions: union-find over edges between claimed endpoints
+    k_region_union<<<NB(ne), 256, 0, s>>>(w.ea, w.eb, w.ew, ne, w.vcls, w.acc, w.rpar);
+    k_region_roots<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, w.acc, rank, rev, ni, w.rpar, w.ridx,
+                                           w.scal + SC_NREG, w.rsad, w.rtop, w.rsize);
+    k_region_tops<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, rank, rev, ni, w.rpar, w.ridx, w.rtop);
+    k_region_label<<<NB(n), 256, 0, s>>>(rank, rev, ni, w.ptr, w.vcls, w.acc, w.rpar, w.ridx, w.reg_of, w.rsize);
+    g_launches += 4;
+    LTS_KCHECK();
+    LTS_TRY(readback(c, SC_NREG, 1));
+    R = c.h_scal[SC_NREG];
+  }
+  {
+    Phase ph(c, LTS_PH_ASSEMBLE);
+    k_region_slots<<<NB(R), 256, 0, s>>>(w.rsize, R, w.rtmp);
+    g_launches++;
+    LTS_TRY(scan_int(w.rtmp, w.rptr, R, w.bsum, w.scal + SC_S, false, s));
+    k_claimed_flags<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.reg_of, w.flagscan);
+    g_launches++;
+    LTS_TRY(scan_int(w.flagscan, w.flagscan, n, w.bsum, w.scal + SC_C, false, s));
+    LTS_TRY(readback(c, SC_S, 2));
+    S = c.h_scal[SC_S];
+    C = c.h_scal[SC_C];
+    LTS_CUDA(cudaMemcpyAsync(w.rptr + R, w.scal + SC_S, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    k_claimed_compact<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.reg_of, w.flagscan, w.ckey, w.cval);
+    g_launches++;
+    LTS_TRY(radix_sort(w.ckey, w.cval, C, bits_for(R - 1), false, w.skey, w.sval, nullptr, w.sb, s));
+    k_place<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, w.loc_of);
+    k_place_saddles<<<NB(R), 256, 0, s>>>(inv, rev, ni, w.rsad, R, w.rptr, w.verts);
+    // schedule: largest region first (stable by region id)
+    k_order_keys<<<NB(R), 256, 0, s>>>(w.rsize, R, (uint32_t *)w.okey);
+    g_launches += 3;
+    LTS_TRY(radix_sort((uint32_t *)w.okey, nullptr, R, 31, false, w.okey2, (uint32_t *)w.order, nullptr, w.sb, s));
+    LTS_KCHECK();
+  }
+  {
+    Phase ph(c, LTS_PH_LOCALIZE);
+    LocArgs A;
+    A.g = c.g; A.rank = rank; A.rev = rev; A.order = w.order; A.R = R; A.rptr = w.rptr;
+    A.verts = w.verts; A.reg_of = w.reg_of; A.loc_of = w.loc_of; A.buf0 = w.buf0; A.buf1 = w.buf1;
+    A.buf2 = w.buf2; A.out = w.out; A.gheap = w.gheap; A.sfl = w.sfl; A.n_iters = w.nit;
+    A.status = w.st; A.max_iter = max_iter; A.queue = w.scal + SC_QUEUE;
+    int blocks = (R + LOC_WARPS - 1) / LOC_WARPS;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    if (c.g.ndim == 2) k_localize<2><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
+    else k_localize<3><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
+    k_loc_stats<<<NB(R), 256, 0, s>>>(w.nit, w.st, w.rsize, R, w.scal + SC_STATS);
+    g_launches += 2;
+    LTS_KCHECK();
+    LTS_TRY(readback(c, SC_STATS, 4));
+    r.n_iter_max = c.h_scal[SC_STATS];
+    r.capped = c.h_scal[SC_STATS + 1];
+    r.largest = c.h_scal[SC_STATS + 3];
+    if (c.h_scal[SC_STATS + 2]) return lts_set_error(LTS_E_LOCALIZE_NO_MIN, "region without an admissible boundary minimum (status 1)");
+  }
+  {
+    Phase ph(c, LTS_PH_INTEGRATE);
+    LTS_CUDA(cudaMemsetAsync(w.delta, 0, sizeof(int) * n, s));
+    k_delta_claimed<<<NB(C), 256, 0, s>>>(w.sval, C, rank, rev, ni, w.delta);
+    k_delta_saddles<<<NB(R), 256, 0, s>>>(w.rsad, w.rsize, R, w.delta);
+    k_count_shared<<<NB(R), 256, 0, s>>>(w.rsad, w.rsize, R, w.delta, w.scal + SC_NSHARED);
+    g_launches += 3;
+    LTS_TRY(scan_int(w.delta, w.D, n, w.bsum, w.scal + SC_TMP, true, s));
+    LTS_TRY(readback(c, SC_NSHARED, 1));
+    int nshared = c.h_scal[SC_NSHARED];
+    r.shared_saddles = nshared;
+    if (nshared) {
+      k_iota<<<NB(R), 256, 0, s>>>(w.okey, R);  // reuse as values
+      g_launches++;
+      LTS_TRY(radix_sort((const uint32_t *)w.rsad, (const uint32_t *)w.okey, R, bits_for(n - 1), false,
+                         w.okey2, w.oval, nullptr, w.sb, s));
+      k_pos_of<<<NB(R), 256, 0, s>>>(w.oval, R, w.sib_rid, w.pos_of);
+      g_launches++;
+    }
+    k_integrate_plain<<<NB(n), 256, 0, s>>>(rank, rev, ni, w.reg_of, w.D, new_rank, new_inv);
+    k_integrate_regions<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.out, w.rsad, w.rsize, w.rtop,
+                                              w.delta, w.D, w.sib_rid, w.pos_of, R, nshared, rev, ni,
+                                              new_rank, new_inv);
+    g_launches += 2;
+    LTS_KCHECK();
+  }
+  if (g) {
+    Phase ph(c, LTS_PH_REALIZE);
+    k_realize<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, g);
+    g_launches++;
+    LTS_KCHECK();
+  }
+  r.regions = R;
+  r.claimed = C;
+  if (rep) *rep = r;
+  if (view) {
+    k_int_to_i64<<<NB(R + 1), 256, 0, s>>>(w.rptr, w.rptr64, R + 1);
+    g_launches++;
+    view->regions = R;
+    view->slots = S;
+    view->region_ptr = w.rptr64;
+    view->region_verts = w.verts;
+    view->local_rank = w.out;
+    view->n_iters = w.nit;
+    view->status = w.st;
+    view->topseed = w.rtop;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// preserve marks
+// ---------------------------------------------------------------------------
+__global__ void k_set_pmark(const int64_t *ids, int64_t cnt, int64_t n, uint8_t bit, uint8_t *pmark, int *bad) {
+  GRID_STRIDE(i, cnt) {
+    int64_t v = ids[i];
+    if (v < 0 || v >= n) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    atomicOr((unsigned *)(pmark + (v & ~(int64_t)3)), (unsigned)bit << (8 * (v & 3)));
+  }
+}
+
+__global__ void k_set_global(const int *inv, int64_t n, int which, uint8_t *pmark) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int v = which == 0 ? inv[0] : inv[n - 1];
+    pmark[v] |= which == 0 ? PM_MIN : PM_MAX;
+  }
+}
+
+__global__ void k_check_pres(const uint8_t *flags, const uint8_t *pmark, int64_t n, int *bad) {
+  GRID_STRIDE(v, n) {
+    uint8_t p = pmark[v], f = flags[v];
+    if (((p & PM_MAX) && !(f & FL_MAX)) || ((p & PM_MIN) && !(f & FL_MIN))) atomicOr(bad, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *lts_version(void) { return "lts_sm100 1.0 (sm_100a)"; }
+const char *lts_last_error(void) { return g_err.c_str(); }
+int64_t lts_kernel_launches(void) { return g_launches; }
+
+int lts_workspace_size(int ndim, const int64_t *dims, size_t *bytes) {
+  if (ndim != 2 && ndim != 3) return lts_set_error(LTS_E_BAD_DIMS, "grid must be 2D or 3D");
+  int64_t n = 1;
+  for (int a = 0; a < ndim; a++) {
+    if (dims[a] < 2) return lts_set_error(LTS_E_BAD_DIMS, "every grid axis needs at least 2 vertices");
+    n *= dims[a];
+  }
+  WS w;
+  *bytes = (size_t)carve(&w, nullptr, ndim, n) + 256;
+  return 0;
+}
+
+static int order_field_impl(Ctx &c, const float *f, int32_t *rank, int32_t *inverse) {
+  WS &w = c.w;
+  Phase ph(c, LTS_PH_ORDER);
+  LTS_CUDA(cudaMemsetAsync(w.sb.nonfinite, 0, sizeof(int), c.s));
+  uint32_t *inv_out = inverse ? (uint32_t *)inverse : w.sval;
+  LTS_TRY(radix_sort((const uint32_t *)f, nullptr, c.n, 32, true, nullptr, inv_out, rank, w.sb, c.s));
+  LTS_KCHECK();
+  LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_TMP, w.sb.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+  LTS_CUDA(cudaStreamSynchronize(c.s));
+  if (c.h_scal[SC_TMP]) return lts_set_error(LTS_E_FIELD_NONFINITE, "scalar field contains NaN or infinite values");
+  return 0;
+}
+
+int lts_order_field(const float *f, int ndim, const int64_t *dims, int32_t *rank, int32_t *inverse,
+                    void *ws, size_t ws_bytes, void *stream) {
+  Ctx c;
+  LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
+  if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
+  return order_field_impl(c, f, rank, inverse);
+}
+
+int lts_classify(const int32_t *rank, int ndim, const int64_t *dims, uint8_t *flags, int16_t *lower,
+                 int16_t *upper, void *stream) {
+  Ctx c;
+  LTS_TRY(setup(c, ndim, dims, nullptr, 0, stream));
+  if ((lower == nullptr) != (upper == nullptr)) return lts_set_error(LTS_E_INVALID, "lower and upper go together");
+  launch_classify(c.g, rank, flags, lower, upper, c.lut, nullptr, PTR_NONE, c.s);
+  LTS_KCHECK();
+  return 0;
+}
+
+int lts_remove_pass(int kind, const int32_t *rank, const int32_t *inverse, const uint8_t *pmark, int ndim,
+                    const int64_t *dims, int32_t max_iterations, int32_t *new_rank, int32_t *new_inverse,
+                    float *g, lts_pass_report_t *rep, lts_regions_view_t *view, void *ws, size_t ws_bytes,
+                    void *stream) {
+  Ctx c;
+  LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
+  if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
+  if (kind != 0 && kind != 1) return lts_set_error(LTS_E_INVALID, "kind must be 0 (maxima) or 1 (minima)");
+  if (max_iterations < 1) max_iterations = 100;
+  return run_pass(c, kind, rank, inverse, pmark, max_iterations, new_rank, new_inverse, g, rep, view);
+}
+
+int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *pres_max, int64_t n_max,
+                 const int64_t *pres_min, int64_t n_min, const int32_t *order, float *g, int32_t *G,
+                 lts_report_t *rep, const lts_options_t *opt, void *ws, size_t ws_bytes, void *stream) {
+  Ctx c;
+  LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
+  if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
+  lts_options_t o{};
+  o.max_iterations = 100;
+  o.restore_interior_extrema = 1;
+  if (opt) o = *opt;
+  if (o.max_iterations < 1) o.max_iterations = 100;
+  c.timing = o.collect_timing != 0;
+  lts_report_t R{};
+  WS &w = c.w;
+  const int64_t n = c.n;
+  cudaStream_t s = c.s;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (c.timing) {
+    t0 = next_event();
+    cudaEventRecord(t0, s);
+  }
+  // A1/A2: order field F
+  if (order) {
+    LTS_CUDA(cudaMemcpyAsync(w.rankA, order, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+    k_scatter_inverse<<<NB(n), 256, 0, s>>>(w.rankA, w.invA, n);
+    g_launches++;
+  } else {
+    LTS_TRY(order_field_impl(c, f, w.rankA, w.invA));
+  }
+  // preserve marks and validation
+  LTS_CUDA(cudaMemsetAsync(w.pmark, 0, (size_t)n, s));
+  LTS_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(int) * SC_N, s));
+  if (n_max > 0) k_set_pmark<<<NB(n_max), 256, 0, s>>>(pres_max, n_max, n, PM_MAX, w.pmark, w.scal + SC_BADPRES);
+  else k_set_global<<<1, 32, 0, s>>>(w.invA, n, 1, w.pmark);
+  if (n_min > 0) k_set_pmark<<<NB(n_min), 256, 0, s>>>(pres_min, n_min, n, PM_MIN, w.pmark, w.scal + SC_BADPRES);
+  else k_set_global<<<1, 32, 0, s>>>(w.invA, n, 0, w.pmark);
+  {
+    Phase ph(c, LTS_PH_CLASSIFY);
+    launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
+  }
+  k_check_pres<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, w.scal + SC_BADPRES);
+  k_copy_canon<<<NB(n), 256, 0, s>>>(f, g, n);
+  g_launches += 4;
+  LTS_KCHECK();
+  LTS_TRY(readback(c, SC_BADPRES, 1));
+  if (c.h_scal[SC_BADPRES]) return lts_set_error(LTS_E_CONSTRAINT_NOT_EXTREMUM, "a preserved vertex is not an extremum of the input order (ConstraintNotExtremum)");
+
+  int *cr = w.rankA, *ci = w.invA, *nr = w.rankB, *ni = w.invB;
+  bool ok = false;
+  int it = 0;
+  for (it = 1; it <= o.max_iterations; it++) {
+    for (int kind = 0; kind < 2; kind++) {
+      lts_pass_report_t pr{};
+      LTS_TRY(run_pass(c, kind, cr, ci, w.pmark, o.max_iterations, nr, ni, g, &pr, nullptr));
+      if (R.n_passes < LTS_MAX_REPORT_PASSES) R.passes[R.n_passes++] = pr;
+      std::swap(cr, nr);
+      std::swap(ci, ni);
+    }
+    // restore (D6) and verify
+    Phase ph(c, LTS_PH_VERIFY);
+    launch_classify(c.g, cr, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
+    LTS_CUDA(cudaMemsetAsync(w.scal + SC_VERIFY, 0, sizeof(int) * 4, s));
+    k_verify<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, w.scal + SC_VERIFY);
+    g_launches++;
+    LTS_KCHECK();
+    LTS_TRY(readback(c, SC_VERIFY, 4));
+    int lost = c.h_scal[SC_VERIFY + 1] + c.h_scal[SC_VERIFY + 3];
+    if (lost && o.restore_interior_extrema) {
+      for (int kind = 0; kind < 2; kind++) {  // minima first, then maxima
+        LTS_CUDA(cudaMemsetAsync(w.scal + SC_LOST, 0, sizeof(int), s));
+        k_lost<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, kind, w.lost, w.scal + SC_LOST);
+        g_launches++;
+        LTS_TRY(readback(c, SC_LOST, 1));
+        int nl = c.h_scal[SC_LOST];
+        if (!nl) continue;
+        std::vector<int> ids(nl);
+        LTS_CUDA(cudaMemcpyAsync(ids.data(), w.lost, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
+        LTS_CUDA(cudaStreamSynchronize(s));
+        std::sort(ids.begin(), ids.end());
+        for (int x : ids) {
+          if (c.g.ndim == 2) k_restore_target<2><<<1, 32, 0, s>>>(c.g, cr, x, kind, w.scal + SC_RESTORE);
+          else k_restore_target<3><<<1, 32, 0, s>>>(c.g, cr, x, kind, w.scal + SC_RESTORE);
+          k_restore_shift<<<NB(n), 256, 0, s>>>(cr, n, x, kind, w.scal + SC_RESTORE);
+          g_launches += 2;
+        }
+        R.restored += nl;
+      }
+      k_scatter_inverse<<<NB(n), 256, 0, s>>>(cr, ci, n);
+      launch_classify(c.g, cr, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
+      LTS_CUDA(cudaMemsetAsync(w.scal + SC_VERIFY, 0, sizeof(int) * 4, s));
+      k_verify<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, w.scal + SC_VERIFY);
+      g_launches += 2;
+      LTS_KCHECK();
+      LTS_TRY(readback(c, SC_VERIFY, 4));
+    }
+    R.extra_max = c.h_scal[SC_VERIFY];
+    R.lost_max = c.h_scal[SC_VERIFY + 1];
+    R.extra_min = c.h_scal[SC_VERIFY + 2];
+    R.lost_min = c.h_scal[SC_VERIFY + 3];
+    if (R.extra_max == 0 && R.lost_max == 0 && R.extra_min == 0 && R.lost_min == 0) {
+      ok = true;
+      break;
+    }
+  }
+  if (it > o.max_iterations) it = o.max_iterations;
+  LTS_CUDA(cudaMemcpyAsync(G, cr, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  R.ok = ok ? 1 : 0;
+  R.outer_iterations = it;
+  if (c.timing) {
+    t1 = next_event();
+    cudaEventRecord(t1, s);
+  }
+  LTS_CUDA(cudaStreamSynchronize(s));
+  if (c.timing) {
+    for (auto &m : c.marks) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, m.second.first, m.second.second);
+      if (m.first >= 0 && m.first < LTS_NUM_PHASES) R.phase_ms[m.first] += ms;
+    }
+    float tot = 0;
+    cudaEventElapsedTime(&tot, t0, t1);
+    R.phase_ms[LTS_PH_TOTAL] = tot;
+  }
+  if (rep) *rep = R;
+  if (!ok) return lts_set_error(LTS_E_VERIFY_FAILED_AT_CAP, "verify_constraints still failing after maxIterations outer iterations");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,260 @@
+"""LTS engine surface (module lts-engine) on the B200 path.
+
+The reference package ships no engine; this module keeps SPEC's
+names and argument meaning.  Every operation is one call into
+liblts_sm100.so (device-resident; no CPU fallback):
+
+  simplify_field(mesh, f, constraints, options) -> (g, G, report)
+  remove_extrema(mesh, F, discardMaxima, discardMinima, options) -> (G, report)
+  discover_regions / remove_pass: one maxima (or minima) pass with its regions
+  verify_constraints(mesh, G, constraints) -> VerifyReport
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .critical import classify_flags, extrema
+from .errors import ConstraintNotExtremum
+from .order import OrderField, ScalarField, ZetaPolicy, compute_order_field, _as_cuda
+from .triangulation import Triangulation
+
+
+@dataclass
+class ConstraintSet:
+    """Preserve sets (SPEC ConstraintSet).  Empty sets get the global extremum."""
+
+    preserveMinima: object = ()
+    preserveMaxima: object = ()
+
+
+@dataclass
+class SimplifyOptions:
+    """SPEC SimplifyOptions.  threadCount has no meaning on
+    the device and is accepted for signature compatibility."""
+
+    zeta: ZetaPolicy = field(default_factory=ZetaPolicy)
+    restoreInteriorExtrema: bool = True
+    maxIterations: int = 100
+    threadCount: int = 0
+    collectTiming: bool = False
+
+
+@dataclass
+class PassReport:
+    kind: str
+    seeds: int
+    regions: int
+    claimed: int
+    largest: int
+    n_iter_max: int
+    capped: int
+    shared_saddles: int
+
+
+@dataclass
+class SimplifyReport:
+    """SPEC SimplifyReport."""
+
+    ok: bool
+    outerIterations: int
+    restored: int
+    passes: list
+    regionCount: int
+    largestRegion: int
+    maxNI: int
+    capped: int
+    linf: Optional[float] = None
+    phase_ms: dict = field(default_factory=dict)
+    extra_max: int = 0
+    lost_max: int = 0
+    extra_min: int = 0
+    lost_min: int = 0
+
+
+@dataclass
+class VerifyReport:
+    ok: bool
+    extra_maxima: torch.Tensor
+    lost_maxima: torch.Tensor
+    extra_minima: torch.Tensor
+    lost_minima: torch.Tensor
+
+
+def _ids(x, device) -> torch.Tensor:
+    if x is None:
+        return torch.empty(0, dtype=torch.int64, device=device)
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device, dtype=torch.int64)
+    else:
+        t = torch.as_tensor(np.asarray(list(x) if isinstance(x, (set, frozenset)) else x,
+                                       dtype=np.int64), device=device)
+    return t.reshape(-1).contiguous()
+
+
+def _report(rep: "N.lts_report_t") -> SimplifyReport:
+    passes = []
+    for i in range(rep.n_passes):
+        p = rep.passes[i]
+        passes.append(PassReport("max" if p.kind == 0 else "min", p.seeds, p.regions, p.claimed,
+                                 p.largest, p.n_iter_max, p.capped, p.shared_saddles))
+    ph = {name: float(rep.phase_ms[i]) for i, name in enumerate(N.PHASES)}
+    return SimplifyReport(
+        ok=bool(rep.ok), outerIterations=int(rep.outer_iterations), restored=int(rep.restored),
+        passes=passes, regionCount=sum(p.regions for p in passes),
+        largestRegion=max([p.largest for p in passes] + [0]),
+        maxNI=max([p.n_iter_max for p in passes] + [0]), capped=sum(p.capped for p in passes),
+        phase_ms=ph, extra_max=int(rep.extra_max), lost_max=int(rep.lost_max),
+        extra_min=int(rep.extra_min), lost_min=int(rep.lost_min))
+
+
+def simplify_raw(mesh: Triangulation, values: torch.Tensor, pres_max: torch.Tensor,
+                 pres_min: torch.Tensor, order: Optional[torch.Tensor] = None,
+                 options: Optional[SimplifyOptions] = None, g_out=None, G_out=None):
+    """Device-tensor entry point: values float32 (cuda), pres_* int64 (cuda).
+    Returns (g float32, G int32 ranks, lts_report_t).  No host copies."""
+    options = options or SimplifyOptions()
+    dev = values.device
+    g = g_out if g_out is not None else torch.empty(mesh.n, dtype=torch.float32, device=dev)
+    G = G_out if G_out is not None else torch.empty(mesh.n, dtype=torch.int32, device=dev)
+    ws = N.workspace(mesh.grid_dims, dev)
+    opt = N.lts_options_t()
+    opt.max_iterations = int(options.maxIterations)
+    opt.restore_interior_extrema = 1 if options.restoreInteriorExtrema else 0
+    opt.collect_timing = 1 if options.collectTiming else 0
+    rep = N.lts_report_t()
+    rc = N.load().lts_simplify(N.ptr(values), mesh.dim, N.dims_arg(mesh.grid_dims), N.ptr(pres_max),
+                               pres_max.numel(), N.ptr(pres_min), pres_min.numel(),
+                               N.ptr(order) if order is not None else None, N.ptr(g), N.ptr(G),
+                               ctypes.byref(rep), ctypes.byref(opt), N.ptr(ws), ws.numel(),
+                               N.stream_ptr())
+    N.check(rc)
+    return g, G, rep
+
+
+def simplify_field(mesh: Triangulation, f, constraints: ConstraintSet,
+                   options: Optional[SimplifyOptions] = None, order: Optional[OrderField] = None):
+    """SPEC.md:348-356.  f: ScalarField (or array-like of n float32 values).
+    Returns (g: ScalarField, G: OrderField, SimplifyReport)."""
+    if not isinstance(f, ScalarField):
+        f = ScalarField(mesh, f)
+    dev = f.values.device
+    pmax = _ids(constraints.preserveMaxima, dev)
+    pmin = _ids(constraints.preserveMinima, dev)
+    g, G, rep = simplify_raw(mesh, f.values, pmax, pmin,
+                             order.rank32 if order is not None else None, options)
+    report = _report(rep)
+    report.linf = float((g - f.values).abs().max()) if mesh.n else 0.0
+    return ScalarField(mesh, g), OrderField(rank32=G), report
+
+
+def remove_extrema(mesh: Triangulation, F: OrderField, discardMaxima, discardMinima,
+                   options: Optional[SimplifyOptions] = None):
+    """SPEC.md:339-347 (black-list form).  Discards must be extrema of F."""
+    dev = F.rank32.device
+    mn, mx = extrema(mesh, F)
+    dmax = _ids(discardMaxima, dev)
+    dmin = _ids(discardMinima, dev)
+    if dmax.numel() and not torch.isin(dmax, mx).all():
+        raise ConstraintNotExtremum("a discard vertex is not a maximum of F")
+    if dmin.numel() and not torch.isin(dmin, mn).all():
+        raise ConstraintNotExtremum("a discard vertex is not a minimum of F")
+    pmax = mx[~torch.isin(mx, dmax)]
+    pmin = mn[~torch.isin(mn, dmin)]
+    dummy = torch.zeros(mesh.n, dtype=torch.float32, device=dev)
+    _, G, rep = simplify_raw(mesh, dummy, pmax.contiguous(), pmin.contiguous(), F.rank32, options)
+    return OrderField(rank32=G), _report(rep)
+
+
+@dataclass
+class PassRegions:
+    """Regions of one pass (SPEC Region list): region_ptr/verts are device
+    arrays in the reference's localize_regions layout ([saddle] + vertices by
+    ascending rank), plus the per-region local orders and N_I."""
+
+    kind: str
+    region_ptr: torch.Tensor
+    region_verts: torch.Tensor
+    local_rank: torch.Tensor
+    n_iters: torch.Tensor
+    status: torch.Tensor
+    topseed: torch.Tensor
+    report: PassReport
+    new_order: OrderField
+
+
+def _view_tensor(ws: torch.Tensor, addr, count, dtype):
+    """Copy `count` elements at device address `addr` (inside the workspace
+    tensor `ws`) into a fresh tensor; the view is only valid until the next call."""
+    if count == 0 or not addr:
+        return torch.empty(0, dtype=dtype, device=ws.device)
+    off = int(addr) - ws.data_ptr()
+    nbytes = count * torch.empty(0, dtype=dtype).element_size()
+    assert 0 <= off and off + nbytes <= ws.numel()
+    return ws[off:off + nbytes].view(dtype).clone()
+
+
+def remove_pass(mesh: Triangulation, F: OrderField, preserve: ConstraintSet, kind: str = "max",
+                max_iterations: int = 100) -> PassRegions:
+    """One maxima pass (discover -> localize -> integrate) or one minima pass
+    (on the reversed order) with its region artefacts."""
+    dev = F.rank32.device
+    pmark = torch.zeros(mesh.n, dtype=torch.uint8, device=dev)
+    pm = _ids(preserve.preserveMaxima, dev)
+    pn = _ids(preserve.preserveMinima, dev)
+    if pm.numel():
+        pmark[pm] |= 2
+    if pn.numel():
+        pmark[pn] |= 1
+    inv = F.inverse32 if F.inverse32 is not None else F.inverse.to(torch.int32)
+    nr = torch.empty_like(F.rank32)
+    ni = torch.empty_like(F.rank32)
+    ws = N.workspace(mesh.grid_dims, dev)
+    rep = N.lts_pass_report_t()
+    view = N.lts_regions_view_t()
+    N.check(N.load().lts_remove_pass(0 if kind == "max" else 1, N.ptr(F.rank32), N.ptr(inv), N.ptr(pmark),
+                                     mesh.dim, N.dims_arg(mesh.grid_dims), int(max_iterations),
+                                     N.ptr(nr), N.ptr(ni), None, ctypes.byref(rep),
+                                     ctypes.byref(view), N.ptr(ws), ws.numel(), N.stream_ptr()))
+    torch.cuda.current_stream().synchronize()
+    R, S = int(view.regions), int(view.slots)
+    pr = PassReport(kind, rep.seeds, rep.regions, rep.claimed, rep.largest, rep.n_iter_max,
+                    rep.capped, rep.shared_saddles)
+    return PassRegions(
+        kind=kind,
+        region_ptr=_view_tensor(ws, view.region_ptr, R + 1 if R else 0, torch.int64),
+        region_verts=_view_tensor(ws, view.region_verts, S, torch.int32),
+        local_rank=_view_tensor(ws, view.local_rank, S, torch.int32),
+        n_iters=_view_tensor(ws, view.n_iters, R, torch.int32),
+        status=_view_tensor(ws, view.status, R, torch.int32),
+        topseed=_view_tensor(ws, view.topseed, R, torch.int32),
+        report=pr, new_order=OrderField(rank32=nr, inverse32=ni))
+
+
+def discover_regions(mesh: Triangulation, F: OrderField, discardMaxima) -> PassRegions:
+    """regions of the maxima pass that discards discardMaxima."""
+    mn, mx = extrema(mesh, F)
+    d = _ids(discardMaxima, F.rank32.device)
+    if d.numel() and not torch.isin(d, mx).all():
+        raise ConstraintNotExtremum("a discard vertex is not a maximum of F")
+    keep = mx[~torch.isin(mx, d)]
+    return remove_pass(mesh, F, ConstraintSet(preserveMinima=mn, preserveMaxima=keep), "max")
+
+
+def verify_constraints(mesh: Triangulation, G: OrderField, constraints: ConstraintSet) -> VerifyReport:
+    """recompute extrema of G and compare with the preserve sets."""
+    dev = G.rank32.device
+    mn, mx = extrema(mesh, G)
+    pm = _ids(constraints.preserveMaxima, dev)
+    pn = _ids(constraints.preserveMinima, dev)
+    extra_max = mx[~torch.isin(mx, pm)]
+    lost_max = pm[~torch.isin(pm, mx)]
+    extra_min = mn[~torch.isin(mn, pn)]
+    lost_min = pn[~torch.isin(pn, mn)]
+    ok = not (extra_max.numel() or lost_max.numel() or extra_min.numel() or lost_min.numel())
+    return VerifyReport(ok, extra_max, lost_max, extra_min, lost_min)

@@ -1,0 +1,181 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle and
+the reference-generated golden fixtures.  Bit-exact for every integer output
+(order fields, counts, regions) and for the float32 field g, whose values are
+copies of input values (contract D1)."""
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2009_00083_b200 as P
+from oracle import lts_oracle as O
+from paper_2009_00083_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+GOLD = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+IDS = [os.path.basename(p)[:-4] for p in GOLD]
+
+
+def _load(p):
+    z = np.load(p)
+    return {k: z[k] for k in z.files}
+
+
+def _mesh(dims):
+    return P.build_grid_triangulation(tuple(int(d) for d in dims))
+
+
+def _cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("path", GOLD, ids=IDS)
+def test_order_and_classify_golden(path):
+    z = _load(path)
+    mesh = _mesh(z["dims"])
+    F = P.compute_order_field(P.ScalarField(mesh, _cu(z["f"])))
+    np.testing.assert_array_equal(F.rank32.cpu().numpy(), z["F_rank"])
+    inv = F.inverse32.cpu().numpy()
+    np.testing.assert_array_equal(inv[z["F_rank"]], np.arange(mesh.n))
+    lo, up = P.classify_all(mesh, F)
+    np.testing.assert_array_equal(lo.cpu().numpy(), z["lower"])
+    np.testing.assert_array_equal(up.cpu().numpy(), z["upper"])
+
+
+def _regions_by_key(ptr, verts, local, nit, top):
+    out = {}
+    for r in range(len(ptr) - 1):
+        seg = verts[ptr[r]:ptr[r + 1]]
+        loc = local[ptr[r]:ptr[r + 1]]
+        out[(int(seg[0]), int(top[r]))] = (tuple(seg.tolist()), tuple(loc.tolist()), int(nit[r]))
+    return out
+
+
+@pytest.mark.parametrize("path", GOLD, ids=IDS)
+def test_first_max_pass_regions_golden(path):
+    z = _load(path)
+    if "max_region_ptr" not in z:
+        pytest.skip("no maxima pass")
+    mesh = _mesh(z["dims"])
+    F = P.order_from_ranks(z["F_rank"])
+    mn, mx = O.extrema(tuple(z["dims"]), z["F_rank"])
+    keep = np.intersect1d(mx, z["pres_max"])
+    pr = P.remove_pass(mesh, F, P.ConstraintSet(preserveMinima=mn, preserveMaxima=keep), "max")
+    got = _regions_by_key(pr.region_ptr.cpu().numpy(), pr.region_verts.cpu().numpy(),
+                          pr.local_rank.cpu().numpy(), pr.n_iters.cpu().numpy(), pr.topseed.cpu().numpy())
+    ref = _regions_by_key(z["max_region_ptr"], z["max_region_verts"], z["max_local"],
+                          z["max_n_iters"], z["max_topseed"])
+    assert got.keys() == ref.keys()
+    for k in ref:
+        assert got[k] == ref[k], k
+    np.testing.assert_array_equal(pr.new_order.rank32.cpu().numpy(), z["G1"])
+
+
+@pytest.mark.parametrize("path", GOLD, ids=IDS)
+def test_simplify_golden(path):
+    z = _load(path)
+    mesh = _mesh(z["dims"])
+    g, G, rep = P.simplify_field(mesh, _cu(z["f"]),
+                                 P.ConstraintSet(preserveMinima=z["pres_min"], preserveMaxima=z["pres_max"]))
+    assert rep.ok == bool(z["ok"])
+    assert rep.outerIterations == int(z["outer"])
+    np.testing.assert_array_equal(G.rank32.cpu().numpy(), z["G_rank"])
+    assert g.values.cpu().numpy().tobytes() == z["g"].tobytes()
+
+
+def _oracle_case(f, kmax, kmin):
+    dims = tuple(f.shape[::-1])
+    f32 = np.ascontiguousarray(f.ravel(), np.float32)
+    rank, _ = O.order_field(f32)
+    mn, mx = O.extrema(dims, rank)
+    pm, pn = S.select_preserved(rank, mx, mn, kmax, kmin)
+    ref = O.simplify(dims, f32, pm, pn)
+    return dims, f32, pm, pn, ref
+
+
+CASES = {
+    "rand2d_300x200": lambda: (np.round(np.random.default_rng(1).random((200, 300)) * 40) / 40, 5, 5),
+    "rand3d_40x36x30": lambda: (np.random.default_rng(2).random((30, 36, 40)), 10, 10),
+    "cfg1_512": lambda: (S.cfg1(0), 16, 1),
+    "cfg1_512_s1": lambda: (S.cfg1(1), 16, 1),
+    "cfg2_64": lambda: (S.cfg2(0, N=64), 64, 1),
+    "cfg3_96": lambda: (S.cfg3(0, N=96), 30, 30),
+    "cfg4_512": lambda: (S.cfg4(0, N=512, ndisk=60), 60, 1),
+    "cfg5_64": lambda: (S.cfg5(0, N=64), 50, 50),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_simplify_vs_oracle(name):
+    f, kmax, kmin = CASES[name]()
+    dims, f32, pm, pn, ref = _oracle_case(np.asarray(f, np.float32), kmax, kmin)
+    mesh = _mesh(dims)
+    g, G, rep = P.simplify_field(mesh, _cu(f32), P.ConstraintSet(preserveMinima=pn, preserveMaxima=pm))
+    assert rep.ok == ref.ok
+    assert rep.outerIterations == ref.outer_iterations
+    np.testing.assert_array_equal(G.rank32.cpu().numpy(), ref.G_rank)
+    assert g.values.cpu().numpy().tobytes() == ref.g.tobytes()
+    # per-pass counts agree with the oracle's passes
+    for a, b in zip(rep.passes, ref.passes):
+        assert (a.regions, a.claimed, a.n_iter_max, a.capped) == (b.regions, b.claimed, b.n_iter_max, b.capped)
+
+
+def test_order_field_edge_values():
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal(97 * 1031).astype(np.float32)
+    f[rng.random(f.size) < 0.1] = 0.0
+    f[rng.random(f.size) < 0.1] = -0.0
+    f[rng.random(f.size) < 0.05] = 1.5
+    f[:7] = np.float32(3.4e38)
+    f[7:9] = np.float32(-3.4e38)
+    f[9] = np.float32(1e-45)
+    f[10] = np.float32(-1e-45)
+    mesh = _mesh((97, 1031))
+    assert mesh.n == f.size
+    F = P.compute_order_field(P.ScalarField(mesh, _cu(f)))
+    rank, inv = O.order_field(f)
+    np.testing.assert_array_equal(F.rank32.cpu().numpy(), rank)
+    np.testing.assert_array_equal(F.inverse32.cpu().numpy(), inv)
+
+
+def test_field_error_on_nonfinite():
+    mesh = _mesh((8, 8))
+    f = np.ones(64, np.float32)
+    f[5] = np.nan
+    with pytest.raises(P.FieldError):
+        P.compute_order_field(P.ScalarField(mesh, _cu(f)))
+
+
+def test_constraint_not_extremum():
+    mesh = _mesh((16, 16))
+    f = np.random.default_rng(0).random(256).astype(np.float32)
+    rank, _ = O.order_field(f)
+    mn, mx = O.extrema((16, 16), rank)
+    not_ext = np.setdiff1d(np.arange(256), np.union1d(mn, mx))[:1]
+    with pytest.raises(P.ConstraintNotExtremum):
+        P.simplify_field(mesh, _cu(f), P.ConstraintSet(preserveMinima=mn[:1], preserveMaxima=not_ext))
+
+
+def test_preserve_all_is_identity():
+    mesh = _mesh((33, 21))
+    f = np.random.default_rng(3).random(mesh.n).astype(np.float32)
+    rank, _ = O.order_field(f)
+    mn, mx = O.extrema((33, 21), rank)
+    g, G, rep = P.simplify_field(mesh, _cu(f), P.ConstraintSet(preserveMinima=mn, preserveMaxima=mx))
+    assert rep.ok and rep.regionCount == 0
+    np.testing.assert_array_equal(G.rank32.cpu().numpy(), rank)
+    assert np.array_equal(g.values.cpu().numpy(), f)
+
+
+def test_idempotence():
+    """simplify(g) with the same constraints returns g, no regions."""
+    f = S.cfg1(2, N=128)
+    dims, f32, pm, pn, ref = _oracle_case(f, 8, 1)
+    mesh = _mesh(dims)
+    cs = P.ConstraintSet(preserveMinima=pn, preserveMaxima=pm)
+    g, G, rep = P.simplify_field(mesh, _cu(f32), cs)
+    g2, G2, rep2 = P.simplify_field(mesh, g.values.clone(), cs, order=G)
+    assert rep2.ok and rep2.regionCount == 0
+    assert torch.equal(g2.values, g.values)

@@ -1,0 +1,79 @@
+"""CPU-only checks of the boundary: the C-ABI library loads and exports every
+symbol declared in include/lts_sm100.h; host-side metadata matches the
+reference tables; the product path refuses to run without a GPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    txt = open(os.path.join(ROOT, "include", "lts_sm100.h")).read()
+    return sorted(set(re.findall(r"\b(lts_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2009_00083_b200 import _native as N
+    L = N.load()
+    names = _declared()
+    assert "lts_simplify" in names and "lts_order_field" in names
+    for name in names:
+        assert hasattr(L, name), name
+    assert L.lts_version().startswith(b"lts_sm100")
+
+
+def test_workspace_size_and_bad_dims():
+    from paper_2009_00083_b200 import _native as N
+    L = N.load()
+    nb = ctypes.c_size_t(0)
+    assert L.lts_workspace_size(3, N.dims_arg((256, 256, 256)), ctypes.byref(nb)) == 0
+    assert nb.value > 16 ** 3
+    assert L.lts_workspace_size(4, N.dims_arg((2, 2, 2)), ctypes.byref(nb)) == N.E_BAD_DIMS
+    assert L.lts_workspace_size(2, N.dims_arg((1, 5)), ctypes.byref(nb)) == N.E_BAD_DIMS
+
+
+def test_link_tables_match_oracle_restatement():
+    from paper_2009_00083_b200 import grid_link_tables
+    from oracle import lts_oracle as O
+    for d in (2, 3):
+        offs, pairs = grid_link_tables(d)
+        o2, p2 = O.grid_tables(d)
+        np.testing.assert_array_equal(offs, o2)
+        np.testing.assert_array_equal(pairs, p2)
+
+
+def test_mesh_errors_and_neighbors():
+    import paper_2009_00083_b200 as P
+    with pytest.raises(P.MeshError):
+        P.build_grid_triangulation((1, 4))
+    with pytest.raises(P.MeshError):
+        P.build_grid_triangulation((2, 2, 2, 2))
+    m = P.build_grid_triangulation((2, 2))
+    assert sorted(m.neighbors(0).tolist()) == [1, 2, 3]  # SPEC.md:45 example
+    m = P.build_grid_triangulation((5, 5))
+    assert sorted(m.neighbors(12).tolist()) == sorted([11, 13, 7, 17, 18, 6])
+    m = P.build_grid_triangulation((3, 3, 3))
+    assert m.degree(13) == 14
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2009_00083_b200 as P
+    m = P.build_grid_triangulation((4, 4))
+    with pytest.raises(Exception):
+        P.ScalarField(m, np.zeros(16, np.float32))
+
+
+def test_synthetic_generators_small():
+    from paper_2009_00083_b200 import synthetic as S
+    a = S.cfg1(0, N=32)
+    b = S.cfg1(0, N=32)
+    assert a.dtype == np.float32 and a.shape == (32, 32) and np.array_equal(a, b)
+    assert S.cfg2(3, N=8).shape == (8, 8, 8)
+    assert S.CONFIGS[3].dims == (256, 256, 256)
