@@ -39,10 +39,18 @@ __device__ __forceinline__ int forest_root(int *p, int x) {
   }
 }
 
+// path halving on the ascent forest (writes only ancestors) ...
 __global__ void k_compress(int *ptr, int64_t n) {
+  GRID_STRIDE(v, n) forest_root(ptr, (int)v);
+}
+
+// ... then read-only root lookup into a separate array: a halving write by a
+// concurrent thread could otherwise overwrite a final root with an ancestor
+__global__ void k_roots(const int *__restrict__ ptr, int64_t n, int *root) {
   GRID_STRIDE(v, n) {
-    int r = forest_root(ptr, (int)v);
-    ptr[v] = r;
+    int x = ptr[v];
+    for (int q = ptr[x]; q != x; q = ptr[x]) x = q;
+    root[v] = x;
   }
 }
 
@@ -186,14 +194,25 @@ __global__ void k_bv_jump(const int *__restrict__ mlist, int nm, const int *__re
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
     if (comp[m] != m || cst[m] != 0) continue;
-    par[m] = forest_root(par, m);
+    forest_root(par, m);
+  }
+}
+
+__global__ void k_bv_roots(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
+                           const uint8_t *__restrict__ cst, const int *__restrict__ par, int *rt) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    if (comp[m] != m || cst[m] != 0) continue;
+    int x = par[m];
+    for (int q = par[x]; q != x; q = par[x]) x = q;
+    rt[m] = x;
   }
 }
 
 // members: tau accumulator and new component; comp is read through a snapshot
 // of the round's roots (par of the old root), so the update order is irrelevant
 __global__ void k_bv_members(const int *__restrict__ mlist, int nm, int *comp,
-                             const uint8_t *__restrict__ cst, const int *__restrict__ par,
+                             const uint8_t *__restrict__ cst, const int *__restrict__ rt,
                              const int *__restrict__ wc, int *acc) {
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
@@ -201,7 +220,7 @@ __global__ void k_bv_members(const int *__restrict__ mlist, int nm, int *comp,
     if (cst[c] != 0) continue;  // preserved or already final
     int w = wc[c];
     if (w < acc[m]) acc[m] = w;
-    comp[m] = par[c];  // root was written by k_bv_jump (par of a root is its root)
+    comp[m] = rt[c];  // chain root of the old component (k_bv_roots)
   }
 }
 

@@ -121,6 +121,10 @@ __device__ void flood(const LocArgs &A, bool asc, int rid, int s, int k, const i
         if (lane == 0) heap_push(heap, size, hkey(kb, p0 + b));
       }
     }
+    // no admissible minimum: the reference's flood extracts nothing and its
+    // label buffer keeps the previous flood's output (_kernels.py:531-552)
+    if (__shfl_sync(0xffffffffu, size, 0) == 0)
+      for (int p = lane; p < k; p += 32) cout[p] = cin[p];
   }
   __syncwarp();
   int e = 0;

@@ -148,7 +148,8 @@ static int set_offsets(int ndim, cudaStream_t s) {
 
 static const uint8_t *lut_ptr(int ndim) {
   void *p = nullptr;
-  cudaGetSymbolAddress(&p, ndim == 2 ? d_lut2 : d_lut3);
+  cudaError_t e = ndim == 2 ? cudaGetSymbolAddress(&p, d_lut2) : cudaGetSymbolAddress(&p, d_lut3);
+  if (e != cudaSuccess) return nullptr;
   return (const uint8_t *)p;
 }
 
@@ -157,7 +158,7 @@ static const uint8_t *lut_ptr(int ndim) {
 // ---------------------------------------------------------------------------
 struct WS {
   // n-sized int32
-  int *rankA, *invA, *rankB, *invB, *ptr, *acc, *comp, *par, *wc, *rpar, *ridx, *reg_of, *loc_of,
+  int *rankA, *invA, *rankB, *invB, *ptr, *M, *rt, *acc, *comp, *par, *wc, *rpar, *ridx, *reg_of, *loc_of,
       *delta, *D, *flagscan, *mlist;
   uint32_t *ckey, *cval, *skey, *sval;
   // region-sized (n+1) int32
@@ -210,7 +211,7 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   int64_t n1 = n + 1, s2 = 2 * n + 2;
   int KH = ndim == 2 ? 3 : 7;
   w->rankA = i32(n); w->invA = i32(n); w->rankB = i32(n); w->invB = i32(n);
-  w->ptr = i32(n); w->acc = i32(n); w->comp = i32(n); w->par = i32(n); w->wc = i32(n);
+  w->ptr = i32(n); w->M = i32(n); w->rt = i32(n); w->acc = i32(n); w->comp = i32(n); w->par = i32(n); w->wc = i32(n);
   w->rpar = i32(n); w->ridx = i32(n); w->reg_of = i32(n); w->loc_of = i32(n);
   w->delta = i32(n); w->D = i32(n); w->flagscan = i32(n); w->mlist = i32(n);
   w->ckey = u32(n); w->cval = u32(n); w->skey = u32(n); w->sval = u32(n);
@@ -320,6 +321,7 @@ static int setup(Ctx &c, int ndim, const int64_t *dims, void *ws, size_t ws_byte
   LTS_TRY(init_tables());
   LTS_TRY(set_offsets(ndim, c.s));
   c.lut = lut_ptr(ndim);
+  if (!c.lut) return lts_set_error(LTS_E_CUDA, "cudaGetSymbolAddress failed for the link LUT");
   if (!g_h_scal) LTS_CUDA(cudaHostAlloc((void **)&g_h_scal, sizeof(int) * SC_N, cudaHostAllocDefault));
   c.h_scal = g_h_scal;
   c.timing = false;
@@ -380,11 +382,12 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     }
     if (nP == 0) return lts_set_error(LTS_E_NO_SADDLE, "every extremum of this kind is discarded: no saddle");
     k_compress<<<NB(n), 256, 0, s>>>(w.ptr, n);
+    k_roots<<<NB(n), 256, 0, s>>>(w.ptr, n, w.M);
     if (c.g.ndim == 2)
-      k_edges<2><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.ptr, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
+      k_edges<2><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
     else
-      k_edges<3><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.ptr, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
-    g_launches += 2;
+      k_edges<3><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
+    g_launches += 3;
     LTS_KCHECK();
     LTS_TRY(readback(c, SC_ECOUNT, 1));
     const int ne = c.h_scal[SC_ECOUNT];
@@ -395,10 +398,11 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       k_bv_hook<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.best, w.par, w.wc, w.scal + SC_ERR);
       k_bv_cycle<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par);
       k_bv_jump<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par);
-      k_bv_members<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par, w.wc, w.acc);
+      k_bv_roots<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par, w.rt);
+      k_bv_members<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.rt, w.wc, w.acc);
       LTS_CUDA(cudaMemsetAsync(w.scal + SC_ACTIVE, 0, sizeof(int), s));
       k_bv_settle<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.scal + SC_ACTIVE);
-      g_launches += 7;
+      g_launches += 8;
       LTS_KCHECK();
       LTS_TRY(readback(c, SC_ACTIVE, 2));
       if (c.h_scal[SC_ERR]) return lts_set_error(LTS_E_NO_SADDLE, "a discarded extremum cannot reach a preserved one");
@@ -409,7 +413,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     k_region_roots<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, w.acc, rank, rev, ni, w.rpar, w.ridx,
                                            w.scal + SC_NREG, w.rsad, w.rtop, w.rsize);
     k_region_tops<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, rank, rev, ni, w.rpar, w.ridx, w.rtop);
-    k_region_label<<<NB(n), 256, 0, s>>>(rank, rev, ni, w.ptr, w.vcls, w.acc, w.rpar, w.ridx, w.reg_of, w.rsize);
+    k_region_label<<<NB(n), 256, 0, s>>>(rank, rev, ni, w.M, w.vcls, w.acc, w.rpar, w.ridx, w.reg_of, w.rsize);
     g_launches += 4;
     LTS_KCHECK();
     LTS_TRY(readback(c, SC_NREG, 1));
