@@ -1,0 +1,370 @@
+"""Benchmark of the full LTS pass (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 3] [--seed 0]
+
+A "step" is one full LTS pass (SPEC simplify_field: order field -> classify ->
+maxima/minima passes -> restore/verify -> realize) over the 256^3 float32
+field of BASELINE config 3, inputs resident in HBM.  Prints ONE JSON line.
+
+  value  whole-job voxels/s, device-timed (CUDA events per step, L2 flushed
+         between steps outside the event window), max over ranks
+  e2e    the same metric through the public API with host buffers: pinned
+         H2D of f + preserve lists, D2H of g and G, inside the timed region
+  roofline  dominant kernel of the step vs MEASURED_PEAKS.json HBM GB/s
+  cpu_baseline  the CPU oracle (C port of the reference kernels + SPEC glue)
+         on a bounded z-slab sample of the same field, rank 0 only
+
+--impl reference runs the CPU oracle port (the reference is Python/numba and
+does not travel to the GPU box) on that sample per step.
+Multi-GPU: one process per GPU (torchrun), independent replicas
+("replicas only"): the path has no data exchange.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simplified voxels/sec (full LTS pass) at 256^3 fp32; kernel HBM GB/s vs peak"
+UNIT = "voxels/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [x for x in sm if x > 0.5 * mx] if mx else sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(f3d: np.ndarray, cfg, nz: int):
+    """Bounded sample of the workload for the CPU baseline: the first nz
+    z-planes of the same field, preserve counts scaled by nz/NZ."""
+    from paper_2009_00083_b200 import synthetic as S
+    from oracle import lts_oracle as O
+    sub = np.ascontiguousarray(f3d[:nz])
+    dims = tuple(sub.shape[::-1])
+    fr = sub.ravel()
+    rank, _ = O.order_field(fr)
+    mn, mx = O.extrema(dims, rank, os.cpu_count())
+    scale = nz / f3d.shape[0]
+    kmax = max(1, int(round(cfg.n_keep_max * scale)))
+    kmin = max(1, int(round(cfg.n_keep_min * scale)))
+    pm, pn = S.select_preserved(rank, mx, mn, kmax, kmin)
+    return dims, fr, pm, pn
+
+
+def run_oracle(dims, fr, pm, pn, threads):
+    from oracle import lts_oracle as O
+    t0 = time.perf_counter()
+    res = O.simplify(dims, fr, pm, pn, nthreads=threads)
+    dt = time.perf_counter() - t0
+    assert res.ok
+    return dt
+
+
+def reference_arm(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from paper_2009_00083_b200 import synthetic as S
+    cfg = S.CONFIGS[args.config]
+    f3d = S.make_field(args.config, args.seed)
+    nz = args.cpu_nz
+    dims, fr, pm, pn = cpu_sample(f3d, cfg, nz)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        run_oracle(dims, fr, pm, pn, threads)
+    ts = [run_oracle(dims, fr, pm, pn, threads) for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    v = fr.size / t
+    sample = (f"first {nz} z-planes of the {cfg.name} field (seed {args.seed}), {fr.size} voxels, "
+              f"preserve {pm.size} max / {pn.size} min; full pass per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} full LTS pass", "grid": list(cfg.dims), "seed": args.seed,
+                   "sample_grid": list(dims)},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-nz", type=int, default=32, help="z-planes in the CPU baseline sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2009_00083_b200 as P
+    from paper_2009_00083_b200 import _native as N
+    from paper_2009_00083_b200 import synthetic as S
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = S.CONFIGS[args.config]
+    f3d = S.make_field(args.config, args.seed)
+    f_host = torch.from_numpy(f3d.ravel()).pin_memory()
+    n = f_host.numel()
+    mesh = P.build_grid_triangulation(cfg.dims)
+    f_dev = f_host.to(dev)
+    # preserve lists: harness work outside the timed region
+    F = P.compute_order_field(P.ScalarField(mesh, f_dev))
+    mn, mx = P.extrema(mesh, F)
+    pm, pn = S.select_preserved(F.rank32.cpu().numpy(), mx.cpu().numpy(), mn.cpu().numpy(),
+                                cfg.n_keep_max, cfg.n_keep_min)
+    pm_d = torch.from_numpy(pm).to(dev)
+    pn_d = torch.from_numpy(pn).to(dev)
+    g = torch.empty(n, dtype=torch.float32, device=dev)
+    G = torch.empty(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    opt_timed = P.SimplifyOptions(collectTiming=True)
+    opt = P.SimplifyOptions()
+
+    def step(o):
+        return P.simplify_raw(mesh, f_dev, pm_d, pn_d, None, o, g, G)
+
+    for _ in range(args.warmup):
+        step(opt)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region -------------------------------------
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    launches0 = N.kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step(opt)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = N.kernel_launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_ms = sum(step_ms)
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        dist.barrier()
+    ms_per_step = t_ms / args.steps
+    value = world * n / (ms_per_step / 1e3)
+
+    # ---- phase breakdown (library CUDA events on the launching stream) ------
+    flush.zero_()
+    _, _, rep = step(opt_timed)
+    phases = {name: round(float(rep.phase_ms[i]), 4) for i, name in enumerate(N.PHASES)}
+    report = P.engine._report(rep)
+
+    # ---- kernel rooflines: order-field sort and classification -------------
+    hbm, peak_kind = peaks()
+    ws = N.workspace(mesh.grid_dims, dev)
+    rk = torch.empty(n, dtype=torch.int32, device=dev)
+    iv = torch.empty(n, dtype=torch.int32, device=dev)
+    fl = torch.empty(n, dtype=torch.uint8, device=dev)
+    L = N.load()
+    dims = N.dims_arg(mesh.grid_dims)
+
+    def timed(fn, reps=10):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    sort_ms = timed(lambda: N.check(L.lts_order_field(N.ptr(f_dev), mesh.dim, dims, N.ptr(rk), N.ptr(iv),
+                                                      N.ptr(ws), ws.numel(), N.stream_ptr())))
+    cls_ms = timed(lambda: N.check(L.lts_classify(N.ptr(rk), mesh.dim, dims, N.ptr(fl), None, None,
+                                                  N.stream_ptr())))
+    # algorithmic bytes per voxel: sort 64 B (hist read 4; pass 1
+    # read 4 write 8; passes 2-3 read 8 write 8; pass 4 read 8, write inverse 4
+    # + rank 4), classification 5 B (rank read 4, flags write 1)
+    sort_gbs = 64.0 * n / (sort_ms * 1e-3) / 1e9
+    cls_gbs = 5.0 * n / (cls_ms * 1e-3) / 1e9
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp))
+    dom = max((k for k in phases if k != "total"), key=lambda k: phases[k])
+    kernels = {
+        "order_sort": {"ms": sort_ms, "bytes_per_voxel": 64, "achieved_gbs": sort_gbs,
+                       "frac": sort_gbs / hbm, "traffic": traffic.get("order_sort")},
+        "classify": {"ms": cls_ms, "bytes_per_voxel": 5, "achieved_gbs": cls_gbs,
+                     "frac": cls_gbs / hbm, "traffic": traffic.get("classify")},
+    }
+    # dominant phase: latency-bound floods / union-find; its algorithmic bytes
+    # are the region data it must touch
+    claimed = sum(p.claimed for p in report.passes)
+    dom_bytes = {"localize": 76.0 * claimed, "discover": 60.0 * n * 2, "order": 64.0 * n,
+                 "classify": 5.0 * n * 6, "integrate": 24.0 * n * 2, "assemble": 28.0 * n * 2,
+                 "realize": 12.0 * claimed, "verify": 6.0 * n}.get(dom, 0.0)
+    dom_gbs = dom_bytes / (phases[dom] * 1e-3) / 1e9 if phases[dom] > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": hbm, "unit": "GB/s",
+                "frac": dom_gbs / hbm, "traffic": traffic.get(dom), "peak_source": peak_kind,
+                "share_of_step": phases[dom] / phases["total"] if phases["total"] else None}
+
+    # ---- end to end through the public API with host buffers ---------------
+    g_host = torch.empty(n, dtype=torch.float32).pin_memory()
+    G_host = torch.empty(n, dtype=torch.int32).pin_memory()
+    pm_h = torch.from_numpy(pm).pin_memory()
+    pn_h = torch.from_numpy(pn).pin_memory()
+    f_in = torch.empty(n, dtype=torch.float32, device=dev)
+    pm_in = torch.empty_like(pm_d)
+    pn_in = torch.empty_like(pn_d)
+
+    def e2e_step():
+        f_in.copy_(f_host, non_blocking=True)
+        pm_in.copy_(pm_h, non_blocking=True)
+        pn_in.copy_(pn_h, non_blocking=True)
+        gg, GG, _ = P.simplify_raw(mesh, f_in, pm_in, pn_in, None, opt, g, G)
+        g_host.copy_(gg, non_blocking=True)
+        G_host.copy_(GG, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e_ms = []
+    for _ in range(max(3, min(args.steps, 5))):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms.append(a.elapsed_time(b))
+    e2e_t = sum(e_ms) / len(e_ms)
+    if world > 1:
+        tt = torch.tensor([e2e_t], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+    e2e = {"value": world * n / (e2e_t / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": 4 * n + 8 * (pm.size + pn.size), "d2h_bytes_per_step": 8 * n,
+           "ms_per_step": e2e_t}
+
+    # ---- CPU baseline (rank 0, N = 1) ---------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        dims_s, fr, pms, pns = cpu_sample(f3d, cfg, args.cpu_nz)
+        threads = os.cpu_count() or 1
+        dt = run_oracle(dims_s, fr, pms, pns, threads)
+        cpu = {"value": fr.size / dt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": (f"first {args.cpu_nz} z-planes of the same field ({fr.size} voxels), "
+                          f"preserve {pms.size} max / {pns.size} min, one full pass, {dt:.1f} s; "
+                          f"OpenMP in classify/localize, discover/sort/realize sequential")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} full LTS pass", "grid": list(cfg.dims), "n": n,
+                       "seed": args.seed, "preserve": [int(pm.size), int(pn.size)],
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed between steps (256 MiB write, outside the per-step events)"},
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
+            "phases_ms": phases, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "report": {"ok": report.ok, "outer": report.outerIterations,
+                       "passes": [p.__dict__ for p in report.passes]},
+            "step_ms": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

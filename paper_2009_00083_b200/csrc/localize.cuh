@@ -39,6 +39,7 @@ struct LocArgs {
   int *n_iters, *status;
   int max_iter;
   int *queue;
+  int qbase;          // first entry of `order` handled by this launch
 };
 
 __device__ __forceinline__ void heap_push(unsigned long long *h, int &size, unsigned long long x) {
@@ -239,8 +240,8 @@ __global__ void __launch_bounds__(32 * LOC_WARPS) k_localize(LocArgs A) {
     int qi = 0;
     if (lane == 0) qi = atomicAdd(A.queue, 1);
     qi = __shfl_sync(0xffffffffu, qi, 0);
-    if (qi >= A.R) break;
-    const int rid = A.order[qi];
+    if (qi + A.qbase >= A.R) break;
+    const int rid = A.order[A.qbase + qi];
     const int lo = A.rptr[rid];
     const int k = A.rptr[rid + 1] - lo;
     const int *verts = A.verts + lo;

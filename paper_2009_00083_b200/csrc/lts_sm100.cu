@@ -22,6 +22,7 @@
 #include "classify.cuh"
 #include "discover.cuh"
 #include "localize.cuh"
+#include "localize_big.cuh"
 #include "integrate.cuh"
 
 namespace lts {
@@ -173,6 +174,8 @@ struct WS {
   int *verts, *buf0, *buf1, *buf2, *out;
   unsigned long long *gheap;
   uint8_t *sfl;
+  int *binv;
+  uint32_t *gbits, *seenw;
   rs::Bufs sb;
   int *bsum;
   int *scal;  // 64 device scalars
@@ -195,6 +198,8 @@ enum {
   SC_BADPRES = 21,
   SC_RESTORE = 24, // 3
   SC_TMP = 28,
+  SC_NBIG = 29,
+  SC_BIGQ = 30,
   SC_N = 64
 };
 
@@ -227,6 +232,9 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->verts = i32(s2); w->buf0 = i32(s2); w->buf1 = i32(s2); w->buf2 = i32(s2); w->out = i32(s2);
   w->gheap = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)s2);
   w->sfl = (uint8_t *)take((size_t)s2);
+  w->binv = i32(3 * n + 8);
+  w->gbits = u32(2 * n + 64);
+  w->seenw = u32(s2);
   w->sb.k1 = u32(n); w->sb.v1 = u32(n); w->sb.k2 = u32(n); w->sb.v2 = u32(n);
   w->sb.status = u32(rs::status_elems(n));
   w->sb.hist = u32(4 * 256);
@@ -343,6 +351,36 @@ __global__ void k_loc_stats(const int *nit, const int *st, const int *rsize, int
   }
 }
 
+__global__ void k_count_big(const int *rsize, int R, int th, int *out) {
+  GRID_STRIDE(r, R) if (rsize[r] + 1 > th) atomicAdd(out, 1);
+}
+
+static cudaStream_t g_side = nullptr;
+static cudaEvent_t g_fork = nullptr, g_join = nullptr;
+static bool g_big_attr = false;
+
+static int big_stream_fork(cudaStream_t s) {
+  if (!g_side) {
+    LTS_CUDA(cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking));
+    LTS_CUDA(cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming));
+    LTS_CUDA(cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming));
+  }
+  if (!g_big_attr) {
+    LTS_CUDA(cudaFuncSetAttribute(k_localize_big<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
+    LTS_CUDA(cudaFuncSetAttribute(k_localize_big<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
+    g_big_attr = true;
+  }
+  LTS_CUDA(cudaEventRecord(g_fork, s));
+  LTS_CUDA(cudaStreamWaitEvent(g_side, g_fork, 0));
+  return 0;
+}
+
+static int big_stream_join(cudaStream_t s) {
+  LTS_CUDA(cudaEventRecord(g_join, g_side));
+  LTS_CUDA(cudaStreamWaitEvent(s, g_join, 0));
+  return 0;
+}
+
 __global__ void k_order_keys(const int *rsize, int R, uint32_t *key) {
   GRID_STRIDE(r, R) key[r] = 0x7fffffffu - (uint32_t)rsize[r];
 }
@@ -448,14 +486,35 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     A.g = c.g; A.rank = rank; A.rev = rev; A.order = w.order; A.R = R; A.rptr = w.rptr;
     A.verts = w.verts; A.reg_of = w.reg_of; A.loc_of = w.loc_of; A.buf0 = w.buf0; A.buf1 = w.buf1;
     A.buf2 = w.buf2; A.out = w.out; A.gheap = w.gheap; A.sfl = w.sfl; A.n_iters = w.nit;
-    A.status = w.st; A.max_iter = max_iter; A.queue = w.scal + SC_QUEUE;
-    int blocks = (R + LOC_WARPS - 1) / LOC_WARPS;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    if (blocks < 1) blocks = 1;
-    if (c.g.ndim == 2) k_localize<2><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
-    else k_localize<3><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
+    A.status = w.st; A.max_iter = max_iter; A.queue = w.scal + SC_QUEUE; A.qbase = 0;
+    // regions are ordered largest first: the first nbig (k > BIG_THRESHOLD) go
+    // to the CTA-batched flood on a side stream, the rest to warp floods
+    k_count_big<<<NB(R), 256, 0, s>>>(w.rsize, R, BIG_THRESHOLD, w.scal + SC_NBIG);
+    g_launches++;
+    LTS_TRY(readback(c, SC_NBIG, 1));
+    const int nbig = c.h_scal[SC_NBIG];
+    if (nbig > 0) {
+      LTS_TRY(big_stream_fork(s));
+      BigArgs B;
+      B.inv = w.binv; B.gbits = w.gbits; B.seenw = w.seenw; B.qbase = 0; B.nbig = nbig;
+      B.queue = w.scal + SC_BIGQ;
+      int gb = nbig < 148 ? nbig : 148;
+      if (c.g.ndim == 2) k_localize_big<2><<<gb, BIG_T, sizeof(BigSmem), g_side>>>(A, B);
+      else k_localize_big<3><<<gb, BIG_T, sizeof(BigSmem), g_side>>>(A, B);
+      g_launches++;
+      LTS_KCHECK();
+    }
+    A.qbase = nbig;
+    if (R > nbig) {
+      int blocks = (R - nbig + LOC_WARPS - 1) / LOC_WARPS;
+      if (blocks > 148 * 8) blocks = 148 * 8;
+      if (c.g.ndim == 2) k_localize<2><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
+      else k_localize<3><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
+      g_launches++;
+    }
+    if (nbig > 0) LTS_TRY(big_stream_join(s));
     k_loc_stats<<<NB(R), 256, 0, s>>>(w.nit, w.st, w.rsize, R, w.scal + SC_STATS);
-    g_launches += 2;
+    g_launches += 1;
     LTS_KCHECK();
     LTS_TRY(readback(c, SC_STATS, 4));
     r.n_iter_max = c.h_scal[SC_STATS];
