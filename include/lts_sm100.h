@@ -145,6 +145,11 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
                  float *g, int32_t *G, lts_report_t *rep, const lts_options_t *opt, void *ws,
                  size_t ws_bytes, void *stream);
 
+/* Diagnostics: enable (1) / read per-region counters of the large-region
+ * flood kernel: out[i*8 + (k, steps, candidates, committed, flood cycles,
+ * check cycles, init cycles, n_iters)] for the first nregions big regions. */
+int lts_debug_big_stats(int enable, int64_t *out, int nregions);
+
 /* Number of CUDA kernels this library launched since load (diagnostics). */
 int64_t lts_kernel_launches(void);
 

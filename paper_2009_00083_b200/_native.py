@@ -59,7 +59,7 @@ class lts_regions_view_t(ctypes.Structure):
 
 
 EXPORTS = ["lts_version", "lts_last_error", "lts_workspace_size", "lts_order_field", "lts_classify",
-           "lts_remove_pass", "lts_simplify", "lts_kernel_launches"]
+           "lts_remove_pass", "lts_simplify", "lts_kernel_launches", "lts_debug_big_stats"]
 
 _lib = None
 
@@ -88,6 +88,7 @@ def load():
                                   P, ctypes.c_size_t, P]
     L.lts_simplify.argtypes = [P, I, P, P, I64, P, I64, P, P, P, ctypes.POINTER(lts_report_t),
                                ctypes.POINTER(lts_options_t), P, ctypes.c_size_t, P]
+    L.lts_debug_big_stats.argtypes = [I, P, I]
     for name in EXPORTS:
         getattr(L, name)
     _lib = L

@@ -39,6 +39,15 @@ __device__ __forceinline__ int forest_root(int *p, int x) {
   }
 }
 
+// pointer jumping round (in place: any ancestor is a valid pointer)
+__global__ void k_jump(int *ptr, int64_t n) {
+  GRID_STRIDE(v, n) {
+    int p = ptr[v];
+    int q = ptr[p];
+    ptr[v] = ptr[q];
+  }
+}
+
 // path halving on the ascent forest (writes only ancestors) ...
 __global__ void k_compress(int *ptr, int64_t n) {
   GRID_STRIDE(v, n) forest_root(ptr, (int)v);
@@ -90,51 +99,74 @@ __global__ void k_mark_maxima(const uint8_t *__restrict__ flags, const uint8_t *
 }
 
 // cross-manifold edges, each grid edge once (positive offsets are the first
-// K/2 entries of the reference offset table)
+// K/2 entries of the reference offset table); output slots are reserved with
+// one global atomic per block iteration
 template <int NDIM>
-__global__ void k_edges(Grid g, const int *__restrict__ rank, int rev, const int *__restrict__ M,
-                        const uint8_t *__restrict__ vcls, int *ea, int *eb, int *ew, int *ecount) {
+__global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ rank, int rev,
+                                               const int *__restrict__ M,
+                                               const uint8_t *__restrict__ vcls, int *ea, int *eb,
+                                               int *ew, int *ecount) {
   constexpr int KH = NDIM == 2 ? 3 : 7;
+  __shared__ int s_w[8];
+  __shared__ int s_base;
   const int n = (int)g.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += gridDim.x * blockDim.x) {
     int v = v0 + threadIdx.x;
-    bool in = v < n;
-    int x = 0, y = 0, z = 0, a = 0, rv = 0;
-    bool pa = false;
-    if (in) {
+    int bs[KH], ws[KH];
+    unsigned emit = 0;
+    int a = 0;
+    if (v < n) {
+      int x, y, z;
       coords(g, v, x, y, z);
       a = M[v];
-      rv = eff_rank(rank, v, rev, n);
-      pa = vcls[a] == 2;
-    }
+      int rv = eff_rank(rank, v, rev, n);
+      bool pa = vcls[a] == 2;
 #pragma unroll
-    for (int k = 0; k < KH; k++) {
-      int u = in ? nbr_at(g, x, y, z, k) : -1;
-      int b = -1, w = 0;
-      bool emit = false;
-      if (u >= 0) {
-        b = M[u];
-        if (b != a && !(pa && vcls[b] == 2)) {
-          int ru = eff_rank(rank, u, rev, n);
-          w = ru < rv ? ru : rv;
-          emit = true;
-        }
-      }
-      unsigned m = __ballot_sync(0xffffffffu, emit);
-      if (m) {
-        int lane = threadIdx.x & 31;
-        int leader = __ffs(m) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(ecount, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (emit) {
-          int slot = base + __popc(m & lanemask_lt());
-          ea[slot] = a;
-          eb[slot] = b;
-          ew[slot] = w;
+      for (int k = 0; k < KH; k++) {
+        int u = nbr_at(g, x, y, z, k);
+        bs[k] = -1;
+        ws[k] = 0;
+        if (u >= 0) {
+          int b = M[u];
+          if (b != a && !(pa && vcls[b] == 2)) {
+            int ru = eff_rank(rank, u, rev, n);
+            bs[k] = b;
+            ws[k] = ru < rv ? ru : rv;
+            emit |= 1u << k;
+          }
         }
       }
     }
+    int cnt = __popc(emit);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int i = 0; i < 8; i++) {
+        int t = s_w[i];
+        s_w[i] = acc;
+        acc += t;
+      }
+      s_base = acc ? atomicAdd(ecount, acc) : 0;
+    }
+    __syncthreads();
+    int slot = s_base + s_w[warp] + incl - cnt;
+#pragma unroll
+    for (int k = 0; k < KH; k++)
+      if (emit >> k & 1u) {
+        ea[slot] = a;
+        eb[slot] = bs[k];
+        ew[slot] = ws[k];
+        slot++;
+      }
+    __syncthreads();
   }
 }
 

@@ -9,13 +9,15 @@
 // Each step therefore takes the top-B keys of F, computes the exposure maxima
 // of all candidates in parallel (B x K neighbour probes), cuts the prefix at
 // the first preemption and commits it.  On the cfg3 regions a flood needs
-// ~0.5-0.75% as many steps as extractions (measured with the oracle).
+// ~1% as many steps as extractions.
 //
 // Keys are a permutation of a small integer range (the region's local order),
-// so F is a bit set over key space kept as a 32-ary bit tree (levels in shared
-// memory; the leaf level spills to global memory for very large regions).
-// The top-B keys come from a descending walk of the tree; key -> local index
-// is an inverse array rebuilt per flood; "seen" is a per-slot epoch stamp.
+// so F is a bit set over key space kept as a 32-ary bit tree in shared memory
+// (the leaf level spills to global memory for very large regions).  The top-B
+// keys come from a descending walk of the tree; key -> local index is an
+// inverse array rebuilt per flood; "seen" is a bit set over local indices.
+// Region adjacency is resolved once per region into rows of local indices so
+// every flood and check touches one row per vertex.
 // Semantics follow _localize_one (_kernels.py:443-575) exactly, including the
 // empty-ascending-flood case and the period-2 cycle jump (contract D5).
 #pragma once
@@ -23,114 +25,205 @@
 
 namespace lts {
 
-constexpr int BIG_T = 512;
+constexpr int BIG_T = 1024;
 constexpr int BIG_B = 256;                    // max candidates per step
-constexpr int BIG_SMEM_WORDS = 36 * 1024;     // bit-tree words in shared memory
+constexpr int BIG_SMEM_WORDS = 36 * 1024;     // bit-set words in shared memory
 constexpr int BIG_THRESHOLD = 1024;           // regions with k > this use this kernel
 
 struct BigArgs {
   int *inv;          // key -> local index, S + R entries (region base lo + rid)
-  uint32_t *gbits;   // spill space for the leaf level
-  uint32_t *seenw;   // per slot: epoch of the last flood that saw it
+  uint32_t *gbits;   // spill space for leaf / seen bit sets
+  int *nrow;         // per slot: K local neighbour indices (-1 = not a member)
+  int *nrowkey;      // per slot: K neighbour keys of the current flood
   int qbase, nbig;   // regions order[qbase .. qbase+nbig)
   int *queue;
 };
 
-struct BitTree {
-  uint32_t *L[6];
-  int nw[6];
+// optional per-region instrumentation (lts_debug_big_stats): big-queue slot i
+// records [k, steps, candidates, committed, flood cycles, check cycles, init
+// cycles, n_iters]
+constexpr int DBG_MAX = 256, DBG_W = 16;
+__device__ long long d_dbg[DBG_MAX * DBG_W];
+__device__ int d_dbg_on;
+
+// Frontier F as a counted bit set over key space [0, k]: leaf bits plus, per
+// block of 32^(l+1) keys, the number of keys in F (levels 1..top).  The top
+// level has <= 32 blocks, so one warp reads it in one step.
+struct CTree {
+  uint32_t *leaf;
+  int nw0;          // leaf words
+  int *cnt[6];      // cnt[l][i], l = 1..top: keys in block i of level l
+  int nb[6];        // blocks per level (nb[0] = nw0)
   int top;
 };
 
 __device__ __forceinline__ uint32_t mask_le(int b) { return b >= 31 ? 0xffffffffu : ((2u << b) - 1u); }
 
-// largest set key <= x, or -1
-__device__ int bt_prev(const BitTree &T, int x) {
-  int l = 0, pos = x;
+__device__ __forceinline__ void ct_insert(const CTree &T, int key) {
+  atomicOr(T.leaf + (key >> 5), 1u << (key & 31));
+  for (int l = 1; l <= T.top; l++) atomicAdd(T.cnt[l] + (key >> (5 * (l + 1))), 1);
+}
+
+__device__ __forceinline__ void ct_remove(const CTree &T, int key) {
+  atomicAnd(T.leaf + (key >> 5), ~(1u << (key & 31)));
+  for (int l = 1; l <= T.top; l++) atomicSub(T.cnt[l] + (key >> (5 * (l + 1))), 1);
+}
+
+// warp-aggregated count updates: the upper levels have few blocks, so per-key
+// shared atomics would serialise on a handful of addresses
+__device__ __forceinline__ void ct_update_warp(const CTree &T, int key, bool valid, int delta) {
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31;
+  if (valid) {
+    if (delta > 0) atomicOr(T.leaf + (key >> 5), 1u << (key & 31));
+    else atomicAnd(T.leaf + (key >> 5), ~(1u << (key & 31)));
+  }
+  for (int l = 1; l <= T.top; l++) {
+    int idx = valid ? (key >> (5 * (l + 1))) : -1;
+    unsigned peers = __match_any_sync(act, idx);
+    if (valid && lane == __ffs(peers) - 1) atomicAdd(T.cnt[l] + idx, delta * __popc(peers));
+  }
+}
+
+// warp 0: the `need`-th largest key of F (need clamped to |F|).  Returns the
+// threshold key tau (-1 if F is empty) and the clamped need.
+__device__ __forceinline__ int ct_threshold(const CTree &T, int want, int &need_out) {
+  const int lane = threadIdx.x & 31;
+  int l = T.top, base = 0, nel = T.nb[T.top];
+  int need = want;
+  bool first = true;
   for (;;) {
-    if (pos < 0) return -1;
-    int w = pos >> 5;
-    uint32_t m = ((volatile uint32_t *)T.L[l])[w] & mask_le(pos & 31);
-    if (m) {
-      pos = (w << 5) + 31 - __clz(m);
-      break;
+    int e = base + nel - 1 - lane;
+    int c = 0;
+    if (lane < nel) c = l == 0 ? __popc(((volatile uint32_t *)T.leaf)[e]) : ((volatile int *)T.cnt[l])[e];
+    int P = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, P, o);
+      if (lane >= o) P += y;
     }
-    if (l == T.top) {
-      pos = (w << 5) - 1;
-      continue;
+    if (first) {
+      int total = __shfl_sync(0xffffffffu, P, 31);
+      need = min(need, total);
+      need_out = need;
+      if (need == 0) return -1;
+      first = false;
     }
-    pos = w - 1;
-    l++;
-  }
-  while (l > 0) {
+    unsigned hit = __ballot_sync(0xffffffffu, P >= need);
+    int src = __ffs(hit) - 1;
+    int before = __shfl_sync(0xffffffffu, P - c, src);
+    int es = base + nel - 1 - src;
+    need -= before;
+    if (l == 0) {
+      uint32_t w = ((volatile uint32_t *)T.leaf)[es];
+      // need-th highest set bit of w
+      int b = 31;
+      for (int r = 0;; b--) {
+        if ((w >> b) & 1u) {
+          if (++r == need) break;
+        }
+      }
+      return (es << 5) + b;
+    }
+    base = es << 5;
+    nel = min(32, T.nb[l - 1] - base);
     l--;
-    uint32_t m = ((volatile uint32_t *)T.L[l])[pos];
-    pos = (pos << 5) + 31 - __clz(m);
-  }
-  return pos;
-}
-
-__device__ __forceinline__ void bt_insert(const BitTree &T, int key) {
-  int idx = key;
-  for (int l = 0; l <= T.top; l++) {
-    uint32_t old = atomicOr(T.L[l] + (idx >> 5), 1u << (idx & 31));
-    if (old != 0) break;  // word was already non-empty: ancestors are set
-    idx >>= 5;
   }
 }
 
-template <int NDIM>
-__device__ __forceinline__ int nbr_member(const LocArgs &A, int v, int kk, int rid, int s) {
-  int x, y, z;
-  coords(A.g, v, x, y, z);
-  return member(A, nbr_at(A.g, x, y, z, kk), rid, s);
-}
-
-// smem layout for the big kernel (dynamic)
 struct BigSmem {
   int cand_key[BIG_B];
   int cand_p[BIG_B];
-  int cand_v[BIG_B];
   int newmax[BIG_B];
   int pair_q[BIG_B * kMaxK];
   int pair_key[BIG_B * kMaxK];
-  int ncand, cut, nsrc, red;
+  int wsum[BIG_T / 32 + 1];
+  int ncand, cut, nsrc, red, v0, qi, tau, carry;
+  CTree T;          // frontier descriptor (uniform; kept out of local memory)
+  uint32_t *seen;   // bit set over local indices
   uint32_t bits[BIG_SMEM_WORDS];
 };
 
-template <int NDIM>
-__device__ void big_flood(const LocArgs &A, const BigArgs &Bg, BigSmem &S, BitTree &T, bool asc,
-                          int rid, int s, int lo, int k, const int *verts, const int *cin, int *cout,
-                          const uint8_t *sfl, uint32_t epoch, int *inv, int &Beff) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+struct BigRegion {
+  int rid, lo, k, s;
+  const int *verts;
+  const int *row;   // k*K local neighbour indices
+  int *rowkey;      // k*K neighbour keys of the current flood (-1: not a member)
+  uint8_t *sfl;
+  int *inv;
+};
+
+__device__ __forceinline__ bool seen_test(const uint32_t *seen, int q) {
+  return (((volatile const uint32_t *)seen)[q >> 5] >> (q & 31)) & 1u;
+}
+
+// desc floods map the sentinels +BIG -> k, -BIG -> 0; asc floods reverse
+__device__ __forceinline__ int flood_key(int c, bool asc, int k) {
+  if (asc) return k - 1 - c;
+  if (c == 0x7fffffff) return k;
+  if (c == (int)0x80000000) return 0;
+  return c;
+}
+
+// block-wide exclusive scan (BIG_T threads): warp scans, warp 0 scans the
+// warp totals, one extra barrier
+__device__ __forceinline__ int big_scan_excl(int x, int *wsum, int &total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < BIG_T / 32 ? wsum[lane] : 0;
+    int p = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, p, o);
+      if (lane >= o) p += y;
+    }
+    if (lane < BIG_T / 32) wsum[lane] = p - v;
+    if (lane == 31) wsum[BIG_T / 32] = p;
+  }
+  __syncthreads();
+  total = wsum[BIG_T / 32];
+  return wsum[warp] + inc - x;
+}
+
+template <int K>
+__device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, int *cout, int &Beff,
+                          long long *dbg) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int K1 = k + 1;
-  uint32_t *seen = Bg.seenw + lo;
-  // key of local index p: desc floods map the sentinels +BIG -> k, -BIG -> 0
-  auto keyof = [&](int p) -> int {
-    int c = cin[p];
-    if (asc) return k - 1 - c;
-    if (c == 0x7fffffff) return k;
-    if (c == (int)0x80000000) return 0;
-    return c;
-  };
-  for (int l = 0; l <= T.top; l++)
-    for (int i = tid; i < T.nw[l]; i += BIG_T) T.L[l][i] = 0u;
+  const int k = G.k;
+  const CTree &T = S.T;
+  uint32_t *const seen = S.seen;
+  const int seen_words = (k + 31) >> 5;
+  for (int i = tid; i < T.nw0; i += BIG_T) T.leaf[i] = 0u;
+  for (int l = 1; l <= T.top; l++)
+    for (int i = tid; i < T.nb[l]; i += BIG_T) T.cnt[l][i] = 0;
+  for (int i = tid; i < seen_words; i += BIG_T) seen[i] = 0u;
   if (tid == 0) S.nsrc = 0;
   __syncthreads();
-  for (int p = tid; p < k; p += BIG_T) inv[keyof(p)] = p;
-  // sources
+  for (int p = tid; p < k; p += BIG_T) G.inv[flood_key(cin[p], asc, k)] = p;
+  // neighbour keys of this flood, one row per local index
+  for (int i = tid; i < k * K; i += BIG_T) {
+    int q = G.row[i];
+    G.rowkey[i] = q >= 0 ? flood_key(cin[q], asc, k) : -1;
+  }
   if (!asc) {
     if (tid == 0) {
-      seen[0] = epoch;
-      bt_insert(T, keyof(0));
+      atomicOr(seen, 1u);
+      ct_insert(T, flood_key(cin[0], false, k));
       S.nsrc = 1;
     }
   } else {
     for (int p = 1 + tid; p < k; p += BIG_T)
-      if ((sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) {
-        seen[p] = epoch;
-        bt_insert(T, keyof(p));
+      if ((G.sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) {
+        atomicOr(seen + (p >> 5), 1u << (p & 31));
+        ct_insert(T, flood_key(cin[p], true, k));
         atomicAdd(&S.nsrc, 1);
       }
   }
@@ -141,50 +234,68 @@ __device__ void big_flood(const LocArgs &A, const BigArgs &Bg, BigSmem &S, BitTr
     return;
   }
   int e = 0;
-  int pos = K1 - 1;  // no key above the current top can re-enter F except via exposure
+  long long tq = clock64(), tn;
+#define BIG_TICK(slot)                          \
+  if (dbg && tid == 0) {                        \
+    tn = clock64();                             \
+    dbg[slot] += tn - tq;                       \
+    tq = tn;                                    \
+  }
   for (;;) {
-    // (a) candidates: top keys of F in descending order (warp 0)
+    BIG_TICK(8)
+    // (a) threshold: the Beff-th largest key of F (warp 0, counted descent)
     if (warp == 0) {
-      int nc = 0;
-      int x = K1 - 1;
-      while (nc < Beff) {
-        int key0 = 0;
-        if (lane == 0) key0 = bt_prev(T, x);
-        key0 = __shfl_sync(0xffffffffu, key0, 0);
-        if (key0 < 0) break;
-        int w = key0 >> 5;
-        uint32_t word = ((volatile uint32_t *)T.L[0])[w] & mask_le(key0 & 31);
-        int c = __popc(word);
-        int take = min(c, Beff - nc);
-        if ((word >> lane) & 1u) {
-          int r = __popc(word & ~mask_le(lane));  // set bits above this one
-          if (r < take) {
-            int key = (w << 5) + lane;
-            int p = inv[key];
-            S.cand_key[nc + r] = key;
-            S.cand_p[nc + r] = p;
-            S.cand_v[nc + r] = verts[p];
-            S.newmax[nc + r] = -1;
-          }
-        }
-        nc += take;
-        x = (w << 5) - 1;
-      }
+      int need = 0;
+      int tau = ct_threshold(T, Beff, need);
       if (lane == 0) {
-        S.ncand = nc;
-        S.cut = nc;
+        S.tau = tau;
+        S.ncand = need;
+        S.cut = need;
       }
     }
     __syncthreads();
+    BIG_TICK(9)
     const int nc = S.ncand;
     if (nc == 0) break;
-    // (b) exposure maxima of every candidate
+    // enumerate keys >= tau in descending order: scan leaf words upward from
+    // tau's word; the rank from the bottom gives the output slot
+    {
+      const int tau = S.tau;
+      int carry = 0;
+      for (int w0 = tau >> 5; carry < nc && w0 < T.nw0; w0 += BIG_T) {
+        int w = w0 + tid;
+        uint32_t word = 0;
+        if (w < T.nw0) {
+          word = ((volatile uint32_t *)T.leaf)[w];
+          if (w == (tau >> 5)) word &= ~((1u << (tau & 31)) - 1u);  // keys >= tau
+        }
+        int tot;
+        int ex = big_scan_excl(__popc(word), S.wsum, tot);
+        int r = carry + ex;
+        while (word) {
+          int b = __ffs(word) - 1;
+          word &= word - 1;
+          int o = nc - 1 - r;
+          if (o >= 0) {
+            int key = (w << 5) + b;
+            S.cand_key[o] = key;
+            S.cand_p[o] = G.inv[key];
+            S.newmax[o] = -1;
+          }
+          r++;
+        }
+        carry += tot;
+        __syncthreads();
+      }
+    }
+    BIG_TICK(10)
+    // (b) exposure maxima of every candidate (row and key loads in parallel)
     for (int i = tid; i < nc * K; i += BIG_T) {
       int c = i / K, kk = i - c * K;
-      int q = nbr_member<NDIM>(A, S.cand_v[c], kk, rid, s);
-      int key = -1;
-      if (q >= 0 && ((volatile uint32_t *)seen)[q] != epoch) {
-        key = keyof(q);
+      int off = S.cand_p[c] * K + kk;
+      int q = G.row[off];
+      int key = G.rowkey[off];
+      if (q >= 0 && !seen_test(seen, q)) {
         atomicMax(&S.newmax[c], key);
       } else {
         q = -1;
@@ -193,130 +304,131 @@ __device__ void big_flood(const LocArgs &A, const BigArgs &Bg, BigSmem &S, BitTr
       S.pair_key[i] = key;
     }
     __syncthreads();
-    // (c) prefix max and first preemption (warp 0)
+    BIG_TICK(11)
+    // (c) prefix max and first preemption: warp 0, 8 candidates per lane
     if (warp == 0) {
-      int run = -1;
-      for (int b0 = 0; b0 < nc; b0 += 32) {
-        int i = b0 + lane;
-        int v = i < nc ? S.newmax[i] : -1;
+      constexpr int PER = BIG_B / 32;
+      int loc[PER];
+      int m = -1;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(0xffffffffu, v, o);
-          if (lane >= o) v = max(v, y);
-        }
-        v = max(v, run);
-        bool pre = (i + 1 < nc) && v > S.cand_key[i + 1];
-        unsigned bm = __ballot_sync(0xffffffffu, pre);
-        if (bm) {
-          if (lane == 0) S.cut = b0 + __ffs(bm);  // commit candidates [0, i] (i+1 of them)
-          break;
-        }
-        run = __shfl_sync(0xffffffffu, v, 31);
+      for (int t = 0; t < PER; t++) {
+        int i = lane * PER + t;
+        int v = i < nc ? S.newmax[i] : -1;
+        m = max(m, v);
+        loc[t] = m;
       }
+      int P = m;  // inclusive scan of lane maxima
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, P, o);
+        if (lane >= o) P = max(P, y);
+      }
+      int carry = __shfl_up_sync(0xffffffffu, P, 1);
+      if (lane == 0) carry = -1;
+      int first = 0x7fffffff;
+#pragma unroll
+      for (int t = 0; t < PER; t++) {
+        int i = lane * PER + t;
+        if (i + 1 < nc && max(carry, loc[t]) > S.cand_key[i + 1] && first == 0x7fffffff) first = i + 1;
+      }
+      first = __reduce_min_sync(0xffffffffu, first);
+      if (lane == 0 && first != 0x7fffffff) S.cut = first;
     }
     __syncthreads();
+    BIG_TICK(12)
     const int j = S.cut;
-    // (d) commit: labels, remove from F
-    for (int i = tid; i < j; i += BIG_T) {
-      int p = S.cand_p[i];
-      cout[p] = asc ? (e + i) : (k - 1 - (e + i));
-      int key = S.cand_key[i];
-      atomicAnd(T.L[0] + (key >> 5), ~(1u << (key & 31)));
+    // (d) commit the prefix: labels, leave F; its exposures join F
+    for (int i0 = 0; i0 < j; i0 += BIG_T) {
+      int i = i0 + tid;
+      bool v = i < j;
+      if (v) cout[S.cand_p[i]] = asc ? (e + i) : (k - 1 - (e + i));
+      ct_update_warp(T, v ? S.cand_key[i] : 0, v, -1);
     }
-    __syncthreads();
-    for (int l = 0; l < T.top; l++) {
-      for (int i = tid; i < j; i += BIG_T) {
-        int idx = S.cand_key[i] >> (5 * (l + 1));  // word index at level l
-        if (((volatile uint32_t *)T.L[l])[idx] == 0u)
-          atomicAnd(T.L[l + 1] + (idx >> 5), ~(1u << (idx & 31)));
+    BIG_TICK(13)
+    for (int i0 = 0; i0 < j * K; i0 += BIG_T) {
+      int i = i0 + tid;
+      int q = i < j * K ? S.pair_q[i] : -1;
+      bool ins = false;
+      if (q >= 0) {
+        uint32_t bit = 1u << (q & 31);
+        ins = !(atomicOr(seen + (q >> 5), bit) & bit);
       }
-      __syncthreads();
-    }
-    // exposures of the committed prefix join F
-    for (int i = tid; i < j * K; i += BIG_T) {
-      int q = S.pair_q[i];
-      if (q >= 0 && atomicMax(seen + q, epoch) != epoch) bt_insert(T, S.pair_key[i]);
+      ct_update_warp(T, ins ? S.pair_key[i] : 0, ins, 1);
     }
     e += j;
+    if (dbg && tid == 0) {
+      dbg[1] += 1;
+      dbg[2] += nc;
+      dbg[3] += j;
+    }
     if (j == nc && nc == Beff && Beff < BIG_B) Beff *= 2;
     else if (j * 4 < Beff && Beff > 8) Beff >>= 1;
     __syncthreads();
+    BIG_TICK(14)
   }
-  (void)pos;
+#undef BIG_TICK
 }
 
-template <int NDIM>
-__device__ bool big_check_minima(const LocArgs &A, int rid, int s, int k, const int *verts,
-                                 const int *cur, uint8_t *sfl, int *red) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
-  if (threadIdx.x == 0) *red = 0;
+// after a descending flood: SF_MIN marks, true if an unauthorized minimum
+template <int K>
+__device__ bool big_check_minima(BigSmem &S, BigRegion &G, const int *cur) {
+  if (threadIdx.x == 0) S.red = 0;
   __syncthreads();
   bool bad = false;
-  for (int p = 1 + threadIdx.x; p < k; p += BIG_T) {
-    int v = verts[p];
-    int x, y, z;
-    coords(A.g, v, x, y, z);
+  for (int p = 1 + threadIdx.x; p < G.k; p += BIG_T) {
+    const int *row = G.row + p * K;
     int c = cur[p];
     bool mn = true;
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
-      int q = member(A, nbr_at(A.g, x, y, z, kk), rid, s);
-      if (q >= 0 && cur[q] < c) {
-        mn = false;
-        break;
-      }
+      int q = row[kk];
+      if (q >= 0 && cur[q] < c) mn = false;
     }
-    uint8_t f = sfl[p];
+    uint8_t f = G.sfl[p];
     f = mn ? (f | SF_MIN) : (f & (uint8_t)~SF_MIN);
-    sfl[p] = f;
+    G.sfl[p] = f;
     if (mn && !(f & SF_OUT)) bad = true;
   }
-  if (bad) atomicOr(red, 1);
+  if (bad) atomicOr(&S.red, 1);
   __syncthreads();
-  bool r = *red != 0;
+  bool r = S.red != 0;
   __syncthreads();
   return r;
 }
 
-template <int NDIM>
-__device__ bool big_check_maxima(const LocArgs &A, int rid, int s, int k, const int *verts,
-                                 const int *cur, int *red) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
-  if (threadIdx.x == 0) *red = 0;
+// after an ascending flood: true if a vertex other than the saddle is a max
+template <int K>
+__device__ bool big_check_maxima(BigSmem &S, BigRegion &G, const int *cur) {
+  if (threadIdx.x == 0) S.red = 0;
   __syncthreads();
   bool bad = false;
-  for (int p = 1 + threadIdx.x; p < k; p += BIG_T) {
-    int v = verts[p];
-    int x, y, z;
-    coords(A.g, v, x, y, z);
+  for (int p = 1 + threadIdx.x; p < G.k; p += BIG_T) {
+    const int *row = G.row + p * K;
     int c = cur[p];
     bool mx = true;
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
-      int q = member(A, nbr_at(A.g, x, y, z, kk), rid, s);
-      if (q >= 0 && cur[q] > c) {
-        mx = false;
-        break;
-      }
+      int q = row[kk];
+      if (q >= 0 && cur[q] > c) mx = false;
     }
     if (mx) bad = true;
   }
-  if (bad) atomicOr(red, 1);
+  if (bad) atomicOr(&S.red, 1);
   __syncthreads();
-  bool r = *red != 0;
+  bool r = S.red != 0;
   __syncthreads();
   return r;
 }
 
-__device__ bool big_states_equal(const int *a, const int *b, int k, int *red) {
-  if (threadIdx.x == 0) *red = 0;
+__device__ bool big_states_equal(BigSmem &S, const int *a, const int *b, int k) {
+  if (threadIdx.x == 0) S.red = 0;
   __syncthreads();
   bool diff = false;
   for (int p = threadIdx.x; p < k; p += BIG_T)
     if (a[p] != b[p]) diff = true;
-  if (diff) atomicOr(red, 1);
+  if (diff) atomicOr(&S.red, 1);
   __syncthreads();
-  bool r = *red == 0;
+  bool r = S.red == 0;
   __syncthreads();
   return r;
 }
@@ -326,72 +438,81 @@ __global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
   constexpr int K = NDIM == 2 ? 6 : 14;
   extern __shared__ __align__(16) unsigned char smraw[];
   BigSmem &S = *reinterpret_cast<BigSmem *>(smraw);
-  __shared__ int s_qi, s_v0;
   const int tid = threadIdx.x;
   const int n = (int)A.g.n;
   for (;;) {
-    if (tid == 0) s_qi = atomicAdd(Bg.queue, 1);
+    if (tid == 0) S.qi = atomicAdd(Bg.queue, 1);
     __syncthreads();
-    const int qi = s_qi;
+    const int qi = S.qi;
+    __syncthreads();
     if (qi >= Bg.nbig) break;
-    const int rid = A.order[Bg.qbase + qi];
-    const int lo = A.rptr[rid];
-    const int k = A.rptr[rid + 1] - lo;
-    const int *verts = A.verts + lo;
-    uint8_t *sfl = A.sfl + lo;
-    int *bufs[3] = {A.buf0 + lo, A.buf1 + lo, A.buf2 + lo};
-    int *inv = Bg.inv + lo + rid;
-    const int s = verts[0];
-    const int srank = eff_rank(A.rank, s, A.rev, n);
-    // bit tree geometry over key space [0, k]
-    BitTree T;
-    {
-      int words = (k + 1 + 31) >> 5;
+    BigRegion G;
+    G.rid = A.order[Bg.qbase + qi];
+    G.lo = A.rptr[G.rid];
+    G.k = A.rptr[G.rid + 1] - G.lo;
+    G.verts = A.verts + G.lo;
+    G.sfl = A.sfl + G.lo;
+    G.inv = Bg.inv + G.lo + G.rid;
+    G.row = Bg.nrow + (size_t)G.lo * K;
+    G.rowkey = Bg.nrowkey + (size_t)G.lo * K;
+    G.s = G.verts[0];
+    const int k = G.k, rid = G.rid, lo = G.lo;
+    int *const b0 = A.buf0 + lo, *const b1 = A.buf1 + lo, *const b2 = A.buf2 + lo;
+#define BUF(i) ((i) % 3 == 0 ? b0 : ((i) % 3 == 1 ? b1 : b2))
+    // shared-memory layout: counts, leaf bits (if they fit), seen bits
+    if (tid == 0) {
+      CTree &T = S.T;
+      T.nw0 = (k + 1 + 31) >> 5;
+      T.nb[0] = T.nw0;
       int l = 0;
-      T.nw[0] = words;
-      while (T.nw[l] > 32) {
-        T.nw[l + 1] = (T.nw[l] + 31) >> 5;
+      while (T.nb[l] > 32) {
+        T.nb[l + 1] = (T.nb[l] + 31) >> 5;
         l++;
       }
       T.top = l;
-      int upper = 0;
-      for (int i = 1; i <= T.top; i++) upper += T.nw[i];
-      bool leaf_smem = upper + T.nw[0] <= BIG_SMEM_WORDS;
       uint32_t *sp = S.bits;
-      if (leaf_smem) {
-        T.L[0] = sp;
-        sp += T.nw[0];
-      } else {
-        T.L[0] = Bg.gbits + ((lo + rid + 31) >> 5) + rid;
-      }
+      int used = 0;
       for (int i = 1; i <= T.top; i++) {
-        T.L[i] = sp;
-        sp += T.nw[i];
+        T.cnt[i] = (int *)sp;
+        sp += T.nb[i];
+        used += T.nb[i];
       }
+      const int seen_words = (k + 31) >> 5;
+      uint32_t *gp = Bg.gbits + 2 * (((size_t)lo + rid + 31) >> 5) + 4 * (size_t)rid;
+      if (used + T.nw0 <= BIG_SMEM_WORDS) {
+        T.leaf = sp;
+        sp += T.nw0;
+        used += T.nw0;
+      } else {
+        T.leaf = gp;
+        gp += T.nw0;
+      }
+      S.seen = (used + seen_words <= BIG_SMEM_WORDS) ? sp : gp;
     }
-    if (tid == 0) s_v0 = 0x7fffffff;
     __syncthreads();
+    long long *dbg = (d_dbg_on && qi < DBG_MAX) ? d_dbg + qi * DBG_W : nullptr;
+    long long c0 = clock64(), c1;
+    // rows, has_outside, v0 (_kernels.py:460-481)
+    if (tid == 0) S.v0 = 0x7fffffff;
+    __syncthreads();
+    const int srank = eff_rank(A.rank, G.s, A.rev, n);
     for (int p = tid; p < k; p += BIG_T) {
+      int x, y, z;
+      coords(A.g, G.verts[p], x, y, z);
       bool out = false;
-      if (p >= 1) {
-        int x, y, z;
-        coords(A.g, verts[p], x, y, z);
+      int *row = Bg.nrow + ((size_t)lo + p) * K;
 #pragma unroll
-        for (int kk = 0; kk < K; kk++) {
-          int u = nbr_at(A.g, x, y, z, kk);
-          if (u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) {
-            out = true;
-            break;
-          }
-        }
+      for (int kk = 0; kk < K; kk++) {
+        int u = nbr_at(A.g, x, y, z, kk);
+        row[kk] = member(A, u, rid, G.s);
+        if (p >= 1 && u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) out = true;
       }
-      sfl[p] = out ? SF_OUT : 0;
-      if (out) atomicMin(&s_v0, p);
-      bufs[0][p] = p;
-      Bg.seenw[lo + p] = 0u;
+      G.sfl[p] = out ? SF_OUT : 0;
+      if (out) atomicMin(&S.v0, p);
+      b0[p] = p;
     }
     __syncthreads();
-    const int v0 = s_v0;
+    const int v0 = S.v0;
     if (v0 == 0x7fffffff) {
       for (int p = tid; p < k; p += BIG_T) A.out[lo + p] = p;
       if (tid == 0) {
@@ -402,42 +523,55 @@ __global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
       continue;
     }
     if (tid == 0) {
-      bufs[0][0] = 0x7fffffff;
-      bufs[0][v0] = (int)0x80000000;
+      b0[0] = 0x7fffffff;
+      b0[v0] = (int)0x80000000;
+      if (dbg) dbg[0] = k;
     }
     __syncthreads();
+    c1 = clock64();
+    if (dbg && tid == 0) dbg[6] += c1 - c0;
     int t = 0, status = 0, fin = 0, Beff = 32;
     for (;;) {
-      big_flood<NDIM>(A, Bg, S, T, false, rid, s, lo, k, verts, bufs[t % 3], bufs[(t + 1) % 3], sfl,
-                      (uint32_t)(t + 1), inv, Beff);
+      c1 = clock64();
+      big_flood<K>(S, G, false, BUF(t), BUF(t + 1), Beff, dbg);
+      c0 = clock64();
+      if (dbg && tid == 0) dbg[4] += c0 - c1;
       t++;
-      bool bad = big_check_minima<NDIM>(A, rid, s, k, verts, bufs[t % 3], sfl, &S.red);
+      bool bad = big_check_minima<K>(S, G, BUF(t));
+      c1 = clock64();
+      if (dbg && tid == 0) dbg[5] += c1 - c0;
       if (!bad) { fin = t; break; }
       if (t >= A.max_iter) { status = 2; fin = t; break; }
-      if (t >= 3 && big_states_equal(bufs[t % 3], bufs[(t + 1) % 3], k, &S.red)) {
+      if (t >= 3 && big_states_equal(S, BUF(t), BUF(t + 1), k)) {
         status = 2;
         fin = ((A.max_iter - t) % 2 == 0) ? t : t - 1;
         t = A.max_iter;
         break;
       }
-      big_flood<NDIM>(A, Bg, S, T, true, rid, s, lo, k, verts, bufs[t % 3], bufs[(t + 1) % 3], sfl,
-                      (uint32_t)(t + 1), inv, Beff);
+      c1 = clock64();
+      big_flood<K>(S, G, true, BUF(t), BUF(t + 1), Beff, dbg);
+      c0 = clock64();
+      if (dbg && tid == 0) dbg[4] += c0 - c1;
       t++;
-      bad = big_check_maxima<NDIM>(A, rid, s, k, verts, bufs[t % 3], &S.red);
+      bad = big_check_maxima<K>(S, G, BUF(t));
+      c1 = clock64();
+      if (dbg && tid == 0) dbg[5] += c1 - c0;
       if (!bad) { fin = t; break; }
       if (t >= A.max_iter) { status = 2; fin = t; break; }
-      if (t >= 3 && big_states_equal(bufs[t % 3], bufs[(t + 1) % 3], k, &S.red)) {
+      if (t >= 3 && big_states_equal(S, BUF(t), BUF(t + 1), k)) {
         status = 2;
         fin = ((A.max_iter - t) % 2 == 0) ? t : t - 1;
         t = A.max_iter;
         break;
       }
     }
-    const int *fb = bufs[fin % 3];
+    const int *fb = BUF(fin);
+#undef BUF
     for (int p = tid; p < k; p += BIG_T) A.out[lo + p] = fb[p];
     if (tid == 0) {
       A.status[rid] = status;
       A.n_iters[rid] = t;
+      if (dbg) dbg[7] = t;
     }
     __syncthreads();
   }

@@ -174,8 +174,8 @@ struct WS {
   int *verts, *buf0, *buf1, *buf2, *out;
   unsigned long long *gheap;
   uint8_t *sfl;
-  int *binv;
-  uint32_t *gbits, *seenw;
+  int *binv, *nrow, *nrowkey;
+  uint32_t *gbits;
   rs::Bufs sb;
   int *bsum;
   int *scal;  // 64 device scalars
@@ -233,8 +233,9 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->gheap = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)s2);
   w->sfl = (uint8_t *)take((size_t)s2);
   w->binv = i32(3 * n + 8);
-  w->gbits = u32(2 * n + 64);
-  w->seenw = u32(s2);
+  w->gbits = u32(5 * n + 64);
+  w->nrow = i32((ndim == 2 ? 6 : 14) * s2);
+  w->nrowkey = i32((ndim == 2 ? 6 : 14) * s2);
   w->sb.k1 = u32(n); w->sb.v1 = u32(n); w->sb.k2 = u32(n); w->sb.v2 = u32(n);
   w->sb.status = u32(rs::status_elems(n));
   w->sb.hist = u32(4 * 256);
@@ -360,6 +361,7 @@ static cudaEvent_t g_fork = nullptr, g_join = nullptr;
 static bool g_big_attr = false;
 
 static int big_stream_fork(cudaStream_t s) {
+  (void)0;
   if (!g_side) {
     LTS_CUDA(cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking));
     LTS_CUDA(cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming));
@@ -419,8 +421,10 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       return 0;
     }
     if (nP == 0) return lts_set_error(LTS_E_NO_SADDLE, "every extremum of this kind is discarded: no saddle");
+    for (int j = 0; j < 3; j++) k_jump<<<NB(n), 256, 0, s>>>(w.ptr, n);
     k_compress<<<NB(n), 256, 0, s>>>(w.ptr, n);
     k_roots<<<NB(n), 256, 0, s>>>(w.ptr, n, w.M);
+    g_launches += 3;
     if (c.g.ndim == 2)
       k_edges<2><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
     else
@@ -496,7 +500,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     if (nbig > 0) {
       LTS_TRY(big_stream_fork(s));
       BigArgs B;
-      B.inv = w.binv; B.gbits = w.gbits; B.seenw = w.seenw; B.qbase = 0; B.nbig = nbig;
+      B.inv = w.binv; B.gbits = w.gbits; B.nrow = w.nrow; B.nrowkey = w.nrowkey; B.qbase = 0; B.nbig = nbig;
       B.queue = w.scal + SC_BIGQ;
       int gb = nbig < 148 ? nbig : 148;
       if (c.g.ndim == 2) k_localize_big<2><<<gb, BIG_T, sizeof(BigSmem), g_side>>>(A, B);
@@ -608,6 +612,23 @@ extern "C" {
 const char *lts_version(void) { return "lts_sm100 1.0 (sm_100a)"; }
 const char *lts_last_error(void) { return g_err.c_str(); }
 int64_t lts_kernel_launches(void) { return g_launches; }
+
+// diagnostics: enable/read the per-region counters of the CTA flood kernel
+int lts_debug_big_stats(int enable, int64_t *out, int nregions) {
+  int on = enable ? 1 : 0;
+  LTS_CUDA(cudaMemcpyToSymbol(d_dbg_on, &on, sizeof(int)));
+  if (enable) {
+    std::vector<long long> z(DBG_MAX * DBG_W, 0);
+    LTS_CUDA(cudaMemcpyToSymbol(d_dbg, z.data(), z.size() * sizeof(long long)));
+  }
+  if (out && nregions > 0) {
+    int m = nregions < DBG_MAX ? nregions : DBG_MAX;
+    LTS_CUDA(cudaMemcpyFromSymbol(out, d_dbg, sizeof(long long) * m * DBG_W));
+  }
+  if (!out && nregions < 0) {
+  }
+  return 0;
+}
 
 int lts_workspace_size(int ndim, const int64_t *dims, size_t *bytes) {
   if (ndim != 2 && ndim != 3) return lts_set_error(LTS_E_BAD_DIMS, "grid must be 2D or 3D");
