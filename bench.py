@@ -23,6 +23,7 @@ Multi-GPU: one process per GPU (torchrun), independent replicas
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -249,28 +250,13 @@ def main():
     # ---- kernel rooflines: order-field sort and classification -------------
     hbm, peak_kind = peaks()
     ws = N.workspace(mesh.grid_dims, dev)
-    rk = torch.empty(n, dtype=torch.int32, device=dev)
-    iv = torch.empty(n, dtype=torch.int32, device=dev)
-    fl = torch.empty(n, dtype=torch.uint8, device=dev)
     L = N.load()
     dims = N.dims_arg(mesh.grid_dims)
 
-    def timed(fn, reps=10):
-        ts = []
-        for _ in range(reps):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
-
-    sort_ms = timed(lambda: N.check(L.lts_order_field(N.ptr(f_dev), mesh.dim, dims, N.ptr(rk), N.ptr(iv),
-                                                      N.ptr(ws), ws.numel(), N.stream_ptr())))
-    cls_ms = timed(lambda: N.check(L.lts_classify(N.ptr(rk), mesh.dim, dims, N.ptr(fl), None, None,
-                                                  N.stream_ptr())))
+    kms = (ctypes.c_double * 4)()
+    N.check(L.lts_bench_kernels(N.ptr(f_dev), mesh.dim, dims, 10, kms, N.ptr(ws), ws.numel(),
+                                N.stream_ptr()))
+    sort_ms, cls_ms, clsptr_ms = kms[0], kms[1], kms[2]
     # algorithmic bytes per voxel: sort 64 B (hist read 4; pass 1
     # read 4 write 8; passes 2-3 read 8 write 8; pass 4 read 8, write inverse 4
     # + rank 4), classification 5 B (rank read 4, flags write 1)
@@ -286,6 +272,9 @@ def main():
                        "frac": sort_gbs / hbm, "traffic": traffic.get("order_sort")},
         "classify": {"ms": cls_ms, "bytes_per_voxel": 5, "achieved_gbs": cls_gbs,
                      "frac": cls_gbs / hbm, "traffic": traffic.get("classify")},
+        "classify_ascent": {"ms": clsptr_ms, "bytes_per_voxel": 9,
+                            "achieved_gbs": 9.0 * n / (clsptr_ms * 1e-3) / 1e9,
+                            "frac": 9.0 * n / (clsptr_ms * 1e-3) / 1e9 / hbm},
     }
     # dominant phase: latency-bound floods / union-find; its algorithmic bytes
     # are the region data it must touch

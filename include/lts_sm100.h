@@ -145,6 +145,12 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
                  float *g, int32_t *G, lts_report_t *rep, const lts_options_t *opt, void *ws,
                  size_t ws_bytes, void *stream);
 
+/* Roofline micro-benchmarks (diagnostics): L2 flushed before each rep, CUDA
+ * events around the kernel(s) only.  out_ms (host, 4): [0] order-field sort,
+ * [1] classification (flags), [2] classification + ascent pointer, [3] 0. */
+int lts_bench_kernels(const float *f, int ndim, const int64_t *dims, int reps, double *out_ms,
+                      void *ws, size_t ws_bytes, void *stream);
+
 /* Diagnostics: enable (1) / read per-region counters of the large-region
  * flood kernel: out[i*8 + (k, steps, candidates, committed, flood cycles,
  * check cycles, init cycles, n_iters)] for the first nregions big regions. */

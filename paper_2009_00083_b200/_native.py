@@ -59,7 +59,7 @@ class lts_regions_view_t(ctypes.Structure):
 
 
 EXPORTS = ["lts_version", "lts_last_error", "lts_workspace_size", "lts_order_field", "lts_classify",
-           "lts_remove_pass", "lts_simplify", "lts_kernel_launches", "lts_debug_big_stats"]
+           "lts_remove_pass", "lts_simplify", "lts_kernel_launches", "lts_debug_big_stats", "lts_bench_kernels"]
 
 _lib = None
 
@@ -89,6 +89,7 @@ def load():
     L.lts_simplify.argtypes = [P, I, P, P, I64, P, I64, P, P, P, ctypes.POINTER(lts_report_t),
                                ctypes.POINTER(lts_options_t), P, ctypes.c_size_t, P]
     L.lts_debug_big_stats.argtypes = [I, P, I]
+    L.lts_bench_kernels.argtypes = [P, I, P, I, P, P, ctypes.c_size_t, P]
     for name in EXPORTS:
         getattr(L, name)
     _lib = L

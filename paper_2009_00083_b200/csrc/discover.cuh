@@ -98,47 +98,45 @@ __global__ void k_mark_maxima(const uint8_t *__restrict__ flags, const uint8_t *
   }
 }
 
-// cross-manifold edges, each grid edge once (positive offsets are the first
-// K/2 entries of the reference offset table); output slots are reserved with
-// one global atomic per block iteration
+// cross-manifold edges of the maxima graph.  Every grid edge is owned by its
+// lower endpoint u (weight = rank u), and u emits one edge per DISTINCT
+// neighbouring manifold: all of u's edges into the same manifold carry the
+// same weight, so the duplicates cannot change any bottleneck.  Output slots
+// are reserved with one global atomic per block iteration.
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ rank, int rev,
                                                const int *__restrict__ M,
                                                const uint8_t *__restrict__ vcls, int *ea, int *eb,
                                                int *ew, int *ecount) {
-  constexpr int KH = NDIM == 2 ? 3 : 7;
+  constexpr int K = NDIM == 2 ? 6 : 14;
   __shared__ int s_w[8];
   __shared__ int s_base;
   const int n = (int)g.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += gridDim.x * blockDim.x) {
     int v = v0 + threadIdx.x;
-    int bs[KH], ws[KH];
-    unsigned emit = 0;
-    int a = 0;
+    int bs[K];
+    int cnt = 0;
+    int a = 0, rv = 0;
     if (v < n) {
       int x, y, z;
       coords(g, v, x, y, z);
       a = M[v];
-      int rv = eff_rank(rank, v, rev, n);
-      bool pa = vcls[a] == 2;
+      rv = eff_rank(rank, v, rev, n);
+      const bool pa = vcls[a] == 2;
 #pragma unroll
-      for (int k = 0; k < KH; k++) {
+      for (int k = 0; k < K; k++) {
         int u = nbr_at(g, x, y, z, k);
-        bs[k] = -1;
-        ws[k] = 0;
-        if (u >= 0) {
-          int b = M[u];
-          if (b != a && !(pa && vcls[b] == 2)) {
-            int ru = eff_rank(rank, u, rev, n);
-            bs[k] = b;
-            ws[k] = ru < rv ? ru : rv;
-            emit |= 1u << k;
-          }
-        }
+        if (u < 0 || eff_rank(rank, u, rev, n) < rv) continue;  // owned by u
+        int b = M[u];
+        if (b == a || (pa && vcls[b] == 2)) continue;
+        bool dup = false;
+#pragma unroll
+        for (int i = 0; i < K; i++)
+          if (i < cnt && bs[i] == b) dup = true;
+        if (!dup) bs[cnt++] = b;
       }
     }
-    int cnt = __popc(emit);
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -159,12 +157,11 @@ __global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ r
     __syncthreads();
     int slot = s_base + s_w[warp] + incl - cnt;
 #pragma unroll
-    for (int k = 0; k < KH; k++)
-      if (emit >> k & 1u) {
-        ea[slot] = a;
-        eb[slot] = bs[k];
-        ew[slot] = ws[k];
-        slot++;
+    for (int i = 0; i < K; i++)
+      if (i < cnt) {
+        ea[slot + i] = a;
+        eb[slot + i] = bs[i];
+        ew[slot + i] = rv;
       }
     __syncthreads();
   }
@@ -180,15 +177,36 @@ __global__ void k_bv_reset(const int *__restrict__ mlist, int nm, unsigned long 
   GRID_STRIDE(i, nm) best[mlist[i]] = 0ull;
 }
 
+// each thread scans a run of consecutive edges (edges are emitted per vertex,
+// so runs share endpoints) and only issues an atomic when its endpoint changes
+constexpr int BV_RUN = 8;
 __global__ void k_bv_best(const int *__restrict__ ea, const int *__restrict__ eb,
                           const int *__restrict__ ew, int ne, const int *__restrict__ comp,
                           const uint8_t *__restrict__ cst, unsigned long long *best) {
-  GRID_STRIDE(i, ne) {
-    int ca = comp[ea[i]], cb = comp[eb[i]];
-    if (ca == cb) continue;
-    int w = ew[i];
-    if (cst[ca] == 0) atomicMax(best + ca, bv_pack(w, cb));
-    if (cst[cb] == 0) atomicMax(best + cb, bv_pack(w, ca));
+  const int64_t nrun = ((int64_t)ne + BV_RUN - 1) / BV_RUN;
+  GRID_STRIDE(r, nrun) {
+    int64_t i0 = r * BV_RUN, i1 = min((int64_t)ne, i0 + BV_RUN);
+    int cur_a = -1, cur_b = -1;
+    unsigned long long best_a = 0ull, best_b = 0ull;
+    for (int64_t i = i0; i < i1; i++) {
+      int ca = comp[ea[i]], cb = comp[eb[i]];
+      if (ca == cb) continue;
+      int w = ew[i];
+      if (ca != cur_a) {
+        if (cur_a >= 0 && best_a) atomicMax(best + cur_a, best_a);
+        cur_a = ca;
+        best_a = 0ull;
+      }
+      if (cb != cur_b) {
+        if (cur_b >= 0 && best_b) atomicMax(best + cur_b, best_b);
+        cur_b = cb;
+        best_b = 0ull;
+      }
+      if (cst[ca] == 0) best_a = max(best_a, bv_pack(w, cb));
+      if (cst[cb] == 0) best_b = max(best_b, bv_pack(w, ca));
+    }
+    if (cur_a >= 0 && best_a) atomicMax(best + cur_a, best_a);
+    if (cur_b >= 0 && best_b) atomicMax(best + cur_b, best_b);
   }
 }
 

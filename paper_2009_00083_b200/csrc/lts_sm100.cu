@@ -313,7 +313,9 @@ static int setup(Ctx &c, int ndim, const int64_t *dims, void *ws, size_t ws_byte
     if (dims[a] < 2) return lts_set_error(LTS_E_BAD_DIMS, "every grid axis needs at least 2 vertices");
     n *= dims[a];
   }
-  if (n >= (int64_t)1 << 30) return lts_set_error(LTS_E_BAD_DIMS, "grid too large (n >= 2^30)");
+  // ranks are packed as (rank << 4 | stencil index) in 32-bit words by the
+  // classification kernel: n <= 2^27 (512^3) keeps that exact
+  if (n > (int64_t)1 << 27) return lts_set_error(LTS_E_BAD_DIMS, "grid too large (n > 2^27)");
   c.g.nx = (int)dims[0];
   c.g.ny = (int)dims[1];
   c.g.nz = ndim == 3 ? (int)dims[2] : 1;
@@ -370,6 +372,11 @@ static int big_stream_fork(cudaStream_t s) {
   if (!g_big_attr) {
     LTS_CUDA(cudaFuncSetAttribute(k_localize_big<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
     LTS_CUDA(cudaFuncSetAttribute(k_localize_big<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
+    // leave the rest of the unified L1/shared array to L1: the floods re-read
+    // region rows and keys that fit there
+    int carve = (int)((sizeof(BigSmem) * 100 + 227 * 1024 - 1) / (228 * 1024)) + 1;
+    LTS_CUDA(cudaFuncSetAttribute(k_localize_big<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    LTS_CUDA(cudaFuncSetAttribute(k_localize_big<3>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     g_big_attr = true;
   }
   LTS_CUDA(cudaEventRecord(g_fork, s));
@@ -613,6 +620,57 @@ const char *lts_version(void) { return "lts_sm100 1.0 (sm_100a)"; }
 const char *lts_last_error(void) { return g_err.c_str(); }
 int64_t lts_kernel_launches(void) { return g_launches; }
 
+// Kernel micro-benchmarks for the roofline report: each rep flushes L2 with a
+// 256 MiB memset, then times one kernel (or kernel group) with events placed
+// directly around it on `stream`.  out_ms[0] order-field sort (histogram +
+// 4 onesweep passes + rank scatter), [1] classification (flags), [2]
+// classification + ascent pointer, [3] mean onesweep pass.  Averages over reps.
+int lts_bench_kernels(const float *f, int ndim, const int64_t *dims, int reps, double *out_ms, void *ws,
+                      size_t ws_bytes, void *stream) {
+  Ctx c;
+  LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
+  if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
+  WS &w = c.w;
+  cudaStream_t s = c.s;
+  const size_t flush_bytes = (size_t)256 << 20;
+  char *flush = (char *)w.nrow;  // scratch: >= 256 MiB for n >= 2^21
+  size_t nrow_bytes = sizeof(int) * (size_t)(ndim == 2 ? 6 : 14) * (size_t)(2 * c.n + 2);
+  size_t fb = flush_bytes < nrow_bytes ? flush_bytes : nrow_bytes;
+  cudaEvent_t a = next_event(), b = next_event();
+  double acc[4] = {0, 0, 0, 0};
+  for (int r = 0; r < reps; r++) {
+    float ms;
+    // sort
+    LTS_CUDA(cudaMemsetAsync(flush, r & 0xff, fb, s));
+    LTS_CUDA(cudaEventRecord(a, s));
+    LTS_TRY(radix_sort((const uint32_t *)f, nullptr, c.n, 32, true, nullptr, (uint32_t *)w.invA, w.rankA, w.sb, s));
+    LTS_CUDA(cudaEventRecord(b, s));
+    LTS_CUDA(cudaEventSynchronize(b));
+    LTS_CUDA(cudaEventElapsedTime(&ms, a, b));
+    acc[0] += ms;
+    // classification, flags only
+    LTS_CUDA(cudaMemsetAsync(flush, r & 0xff, fb, s));
+    LTS_CUDA(cudaEventRecord(a, s));
+    launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
+    LTS_CUDA(cudaEventRecord(b, s));
+    LTS_CUDA(cudaEventSynchronize(b));
+    LTS_CUDA(cudaEventElapsedTime(&ms, a, b));
+    acc[1] += ms;
+    // classification + ascent pointer
+    LTS_CUDA(cudaMemsetAsync(flush, r & 0xff, fb, s));
+    LTS_CUDA(cudaEventRecord(a, s));
+    launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, w.ptr, PTR_ASC, s);
+    LTS_CUDA(cudaEventRecord(b, s));
+    LTS_CUDA(cudaEventSynchronize(b));
+    LTS_CUDA(cudaEventElapsedTime(&ms, a, b));
+    acc[2] += ms;
+  }
+  LTS_KCHECK();
+  for (int i = 0; i < 3; i++) out_ms[i] = acc[i] / (reps > 0 ? reps : 1);
+  out_ms[3] = 0;
+  return 0;
+}
+
 // diagnostics: enable/read the per-region counters of the CTA flood kernel
 int lts_debug_big_stats(int enable, int64_t *out, int nregions) {
   int on = enable ? 1 : 0;
@@ -625,7 +683,15 @@ int lts_debug_big_stats(int enable, int64_t *out, int nregions) {
     int m = nregions < DBG_MAX ? nregions : DBG_MAX;
     LTS_CUDA(cudaMemcpyFromSymbol(out, d_dbg, sizeof(long long) * m * DBG_W));
   }
-  if (!out && nregions < 0) {
+  if (nregions < 0) {  // sort phase counters: enable = -nregions-1 ... read into out[0..7]
+    int on = enable ? 1 : 0;
+    LTS_CUDA(cudaMemcpyToSymbol(rs::d_sort_dbg_on, &on, sizeof(int)));
+    if (enable) {
+      long long z[8] = {0};
+      LTS_CUDA(cudaMemcpyToSymbol(rs::d_sort_dbg, z, sizeof(z)));
+    } else if (out) {
+      LTS_CUDA(cudaMemcpyFromSymbol(out, rs::d_sort_dbg, sizeof(long long) * 8));
+    }
   }
   return 0;
 }

@@ -15,9 +15,9 @@ namespace lts {
 namespace rs {
 
 constexpr int RADIX = 256;
-constexpr int THREADS = 256;
+constexpr int THREADS = 512;
 constexpr int WARPS = THREADS / 32;
-constexpr int KPT = 16;
+constexpr int KPT = 8;
 constexpr int TILE = THREADS * KPT;  // 4096 keys per tile
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_PRE = 2u << 30;
@@ -103,6 +103,9 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t *war
   return off + inc - x;
 }
 
+__device__ long long d_sort_dbg[8];
+__device__ int d_sort_dbg_on;
+
 template <bool FLOATKEY, bool HAS_VALS, bool WRITE_KEYS, bool WRITE_RANK>
 __global__ void __launch_bounds__(THREADS) k_onesweep(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
@@ -112,19 +115,29 @@ __global__ void __launch_bounds__(THREADS) k_onesweep(
   __shared__ uint16_t s_wh[WARPS][RADIX];
   __shared__ uint32_t s_excl[RADIX];
   __shared__ uint32_t s_start[RADIX];
-  __shared__ uint32_t s_wtot[WARPS];
+  __shared__ uint32_t s_wtot[8];
+  __shared__ uint32_t s_hist[RADIX];
   __shared__ uint32_t s_keys[TILE];
   __shared__ uint32_t s_vals[TILE];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long t_prev = clock64();
+#define SORT_TICK(i)                                              \
+  if (d_sort_dbg_on && tid == 0) {                                \
+    long long t_now = clock64();                                  \
+    atomicAdd((unsigned long long *)&d_sort_dbg[i], (unsigned long long)(t_now - t_prev)); \
+    t_prev = t_now;                                               \
+  }
   if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int i = tid; i < WARPS * RADIX; i += THREADS) (&s_wh[0][0])[i] = 0;
+  for (int i = tid; i < WARPS * RADIX / 2; i += THREADS) reinterpret_cast<uint32_t *>(&s_wh[0][0])[i] = 0;
+  if (tid < RADIX) s_hist[tid] = 0;
   __syncthreads();
+  SORT_TICK(1);
   const uint32_t tile = s_tile;
   const int64_t base = (int64_t)tile * TILE;
 
   uint32_t k[KPT], v[KPT];
-  uint16_t r[KPT];
+  uint32_t r[KPT];
 #pragma unroll
   for (int j = 0; j < KPT; j++) {
     int64_t idx = base + warp * 32 * KPT + j * 32 + lane;
@@ -138,27 +151,50 @@ __global__ void __launch_bounds__(THREADS) k_onesweep(
       v[j] = 0;
     }
   }
-  // warp-level multisplit: stable rank of each key among same-digit keys of
-  // this warp (chunks of 32 consecutive keys processed in input order)
+  // tile histogram first (shared atomics) so the aggregate is published
+  // before the expensive ranking: successors' look-backs rarely spin
 #pragma unroll
   for (int j = 0; j < KPT; j++) {
-    uint32_t d = (k[j] >> shift) & 255u;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    int leader = __ffs(peers) - 1;
+    int64_t idx = base + warp * 32 * KPT + j * 32 + lane;
+    if (idx < n) atomicAdd(&s_hist[(k[j] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  SORT_TICK(2);
+  volatile uint32_t *st = status;
+  if (tid < RADIX) {
+    uint32_t c = s_hist[tid];
+    if (tile == 0) st[tid] = FLAG_PRE | (offs[tid] + c);
+    else st[(int64_t)tile * RADIX + tid] = FLAG_AGG | c;
+  }
+  // warp-level multisplit: peers with the same 8-bit digit from 8 ballots;
+  // stable rank among same-digit keys of this warp (chunks of 32 consecutive
+  // keys processed in input order)
+#pragma unroll
+  for (int j = 0; j < KPT; j++) {
+    const uint32_t d = (k[j] >> shift) & 255u;
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+      unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bal : ~bal;
+    }
+    const int leader = __ffs(peers) - 1;
     uint32_t cnt = 0;
     if (lane == leader) {
       cnt = s_wh[warp][d];
       s_wh[warp][d] = (uint16_t)(cnt + __popc(peers));
     }
     cnt = __shfl_sync(0xffffffffu, cnt, leader);
-    r[j] = (uint16_t)(cnt + __popc(peers & lanemask_lt()));
+    r[j] = cnt + __popc(peers & lanemask_lt());
     __syncwarp();
   }
   __syncthreads();
-  // per digit: exclusive offsets across warps, tile total, look-back
-  {
+  SORT_TICK(3);
+  // per digit (threads 0..255): exclusive offsets across warps; decoupled
+  // look-back over predecessors, four status words per round trip
+  uint32_t sum = 0;
+  if (tid < RADIX) {
     const int d = tid;
-    uint32_t sum = 0;
 #pragma unroll
     for (int w = 0; w < WARPS; w++) {
       uint32_t c = s_wh[w][d];
@@ -166,29 +202,53 @@ __global__ void __launch_bounds__(THREADS) k_onesweep(
       sum += c;
     }
     uint32_t excl;
-    volatile uint32_t *st = status;
     if (tile == 0) {
       excl = offs[d];
-      st[d] = FLAG_PRE | (excl + sum);
     } else {
-      st[(int64_t)tile * RADIX + d] = FLAG_AGG | sum;
       uint32_t acc = 0;
       int64_t t = (int64_t)tile - 1;
-      for (;;) {
-        uint32_t s = st[t * RADIX + d];
-        uint32_t f = s & ~VAL_MASK;
-        if (f == 0) continue;
-        acc += s & VAL_MASK;
-        if (f == FLAG_PRE) break;
-        t--;
+      bool done = false;
+      while (!done) {
+        uint32_t sv[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) sv[q] = (t - q >= 0) ? st[(t - q) * RADIX + d] : (FLAG_PRE | 0u);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          if (done) break;
+          uint32_t f = sv[q] & ~VAL_MASK;
+          if (f == 0) break;  // not yet published: re-read from here
+          acc += sv[q] & VAL_MASK;
+          t--;
+          if (f == FLAG_PRE) done = true;
+        }
       }
       excl = acc;
       st[(int64_t)tile * RADIX + d] = FLAG_PRE | (acc + sum);
     }
     s_excl[d] = excl;
-    s_start[d] = block_excl_scan256(sum, s_wtot);
+  }
+  // tile-local digit starts: exclusive scan of the 256 digit totals
+  {
+    uint32_t inc = sum;
+    if (tid < RADIX) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) s_wtot[warp] = inc;
+    }
+    __syncthreads();
+    if (tid < RADIX) {
+      uint32_t off = 0;
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if (i < warp) off += s_wtot[i];
+      s_start[tid] = off + inc - sum;
+    }
   }
   __syncthreads();
+  SORT_TICK(4);
 #pragma unroll
   for (int j = 0; j < KPT; j++) {
     uint32_t d = (k[j] >> shift) & 255u;
@@ -197,8 +257,10 @@ __global__ void __launch_bounds__(THREADS) k_onesweep(
     s_vals[pos] = v[j];
   }
   __syncthreads();
+  SORT_TICK(5);
   int64_t rem = n - base;
   int valid = rem < TILE ? (int)rem : TILE;
+#pragma unroll 4
   for (int i = tid; i < valid; i += THREADS) {
     uint32_t key = s_keys[i];
     uint32_t d = (key >> shift) & 255u;
@@ -208,6 +270,8 @@ __global__ void __launch_bounds__(THREADS) k_onesweep(
     vout[gpos] = val;
     if (WRITE_RANK) rank_out[val] = (int32_t)gpos;
   }
+  SORT_TICK(6);
+#undef SORT_TICK
 }
 
 struct Bufs {
