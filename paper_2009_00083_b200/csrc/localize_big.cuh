@@ -472,13 +472,21 @@ __global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
       T.top = l;
       uint32_t *sp = S.bits;
       int used = 0;
-      for (int i = 1; i <= T.top; i++) {
-        T.cnt[i] = (int *)sp;
-        sp += T.nb[i];
-        used += T.nb[i];
-      }
       const int seen_words = (k + 31) >> 5;
-      uint32_t *gp = Bg.gbits + 2 * (((size_t)lo + rid + 31) >> 5) + 4 * (size_t)rid;
+      uint32_t *gp = Bg.gbits + 3 * (((size_t)lo + rid + 31) >> 5) + 8 * (size_t)rid;
+      int ncnt = 0;
+      for (int i = 1; i <= T.top; i++) ncnt += T.nb[i];
+      const bool cnt_smem = ncnt <= BIG_SMEM_WORDS;  // else every level in global
+      for (int i = 1; i <= T.top; i++) {
+        if (cnt_smem) {
+          T.cnt[i] = (int *)sp;
+          sp += T.nb[i];
+          used += T.nb[i];
+        } else {
+          T.cnt[i] = (int *)gp;
+          gp += T.nb[i];
+        }
+      }
       if (used + T.nw0 <= BIG_SMEM_WORDS) {
         T.leaf = sp;
         sp += T.nw0;

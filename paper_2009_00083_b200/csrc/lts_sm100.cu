@@ -233,7 +233,7 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->gheap = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)s2);
   w->sfl = (uint8_t *)take((size_t)s2);
   w->binv = i32(3 * n + 8);
-  w->gbits = u32(5 * n + 64);
+  w->gbits = u32(6 * n + 64);
   w->nrow = i32((ndim == 2 ? 6 : 14) * s2);
   w->nrowkey = i32((ndim == 2 ? 6 : 14) * s2);
   w->sb.k1 = u32(n); w->sb.v1 = u32(n); w->sb.k2 = u32(n); w->sb.v2 = u32(n);
