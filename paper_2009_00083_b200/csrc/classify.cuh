@@ -21,8 +21,8 @@ namespace lts {
 
 enum { PTR_NONE = 0, PTR_ASC = 1, PTR_DESC = 2 };
 
-constexpr int CL_TX = 32, CL_TY = 8, CL_ZC = 16;
-constexpr int CL_PX = CL_TX + 2, CL_PY = CL_TY + 2;
+constexpr int CL_TX = 32, CL_TY = 8, CL_VY = 2, CL_ZC = 16;  // thread owns CL_VY rows
+constexpr int CL_PX = CL_TX + 2, CL_PY = CL_TY * CL_VY + 2;
 
 // compile-time copy of the reference offset tables (triangulation.py:32-45)
 template <int NDIM>
@@ -44,8 +44,25 @@ struct Stencil {
   }
 };
 
+// Thread layout: 16 x 16 threads, each owns the voxel pair (x, x+1) of one
+// row of a 32 x 16 (x, y) tile and marches in z.  Shared-memory rows are
+// padded so the pair sits at an even index: one 64-bit load fetches both
+// centres / both same-column neighbours, and the 14-neighbour stencil of the
+// pair needs 7 paired + 8 scalar loads.  Flags use 3-input min/max
+// (VIMNMX3): invalid neighbours hold -1, which is never the signed max and
+// always the unsigned max; packing (rank << 4 | k) keeps the arg-extremum.
+constexpr int CP_TX = 16, CP_TY = 16, CP_RY = 2, CP_ZC = 16;  // thread: 2 x-pairs rows
+constexpr int CP_W = 2 * CP_TX;           // tile width (voxels)
+constexpr int CP_PITCH = CP_W + 4;         // padded smem row: [pad, x0-1 .. x0+32, pad]
+constexpr int CP_ROWS = CP_TY * CP_RY + 2;
+constexpr int CP_RING = 5;  // planes z-1..z+1 read, z+2 written: one barrier per plane
+
+struct Nb2 {  // the 14 stencil values of one voxel, reference offset order
+  int v[14];
+};
+
 template <int NDIM, bool COUNTS, int PTR>
-__global__ void __launch_bounds__(CL_TX *CL_TY) k_classify_tile(Grid g, const int32_t *__restrict__ rank,
+__global__ void __launch_bounds__(CP_TX *CP_TY) k_classify_tile(Grid g, const int32_t *__restrict__ rank,
                                                              uint8_t *__restrict__ flags,
                                                              int16_t *__restrict__ lower,
                                                              int16_t *__restrict__ upper,
@@ -53,135 +70,172 @@ __global__ void __launch_bounds__(CL_TX *CL_TY) k_classify_tile(Grid g, const in
                                                              int32_t *__restrict__ ptr) {
   using St = Stencil<NDIM>;
   constexpr int K = St::K;
-  constexpr int NP = NDIM == 2 ? 1 : 3;
-  __shared__ int pl[NP][CL_PY * CL_PX];
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * CL_TX + tx;
-  const int x0 = blockIdx.x * CL_TX, y0 = blockIdx.y * CL_TY;
-  const int x = x0 + tx, y = y0 + ty;
+  constexpr int NP = NDIM == 2 ? 1 : CP_RING;
+  __shared__ __align__(16) int pl[NP][CP_ROWS * CP_PITCH];
+  const int tid = threadIdx.y * CP_TX + threadIdx.x;
+  const int x0 = blockIdx.x * CP_W, y0 = blockIdx.y * (CP_TY * CP_RY);
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const int64_t sxy = (int64_t)nx * ny;
-  // each thread owns <= 2 halo-tile elements; plane z+1 is prefetched into
-  // registers one iteration ahead so HBM latency overlaps the stencil work
-  constexpr int NE = CL_PY * CL_PX, NT = CL_TX * CL_TY;
-  int gofs[2];
-  bool gin[2];
+  constexpr int NE = CP_ROWS * (CP_W + 2), NT = CP_TX * CP_TY, NEPT = (NE + NT - 1) / NT;
+  int gofs[NEPT], sofs[NEPT];
+  bool gin[NEPT], sin_[NEPT];
 #pragma unroll
-  for (int e = 0; e < 2; e++) {
+  for (int e = 0; e < NEPT; e++) {
     int i = tid + e * NT;
-    int py = i / CL_PX, px = i - py * CL_PX;
+    int py = i / (CP_W + 2), px = i - py * (CP_W + 2);
     int gx = x0 + px - 1, gy = y0 + py - 1;
-    gin[e] = i < NE && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+    sin_[e] = i < NE;
+    gin[e] = sin_[e] && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
     gofs[e] = gin[e] ? gy * nx + gx : 0;
+    sofs[e] = py * CP_PITCH + px + 1;
   }
   auto fetch = [&](int z, int *reg) {
 #pragma unroll
-    for (int e = 0; e < 2; e++)
+    for (int e = 0; e < NEPT; e++)
       reg[e] = (gin[e] && z >= 0 && z < nz) ? __ldg(rank + (int64_t)z * sxy + gofs[e]) : -1;
   };
   auto put = [&](int buf, const int *reg) {
 #pragma unroll
-    for (int e = 0; e < 2; e++)
-      if (tid + e * NT < NE) pl[buf][tid + e * NT] = reg[e];
+    for (int e = 0; e < NEPT; e++)
+      if (sin_[e]) pl[buf][sofs[e]] = reg[e];
   };
-  const int zb = NDIM == 2 ? 0 : blockIdx.z * CL_ZC;
-  const int ze = NDIM == 2 ? 1 : min(nz, zb + CL_ZC);
-  int nxt[2], nx2[2], nx3[2];
-  if (NDIM == 3) {
-    int a[2];
-    fetch(zb - 1, a);
-    put(0, a);
-    fetch(zb, a);
-    put(1, a);
-    fetch(zb + 1, nxt);
-    fetch(zb + 2, nx2);
-    fetch(zb + 3, nx3);
-  } else {
-    int a[2];
-    fetch(0, a);
-    put(0, a);
-  }
-  const int c = (ty + 1) * CL_PX + (tx + 1);
-  int r3 = 0;  // (z - zb) % 3
-  for (int z = zb; z < ze; z++) {
-    // ring buffer: plane z-1 in slot r3, z in r3+1, z+1 in r3+2 (mod 3)
-    const int s1 = r3 == 2 ? 0 : r3 + 1;
-    const int s2 = s1 == 2 ? 0 : s1 + 1;
+  const int zb = NDIM == 2 ? 0 : blockIdx.z * CP_ZC;
+  const int ze = NDIM == 2 ? 1 : min(nz, zb + CP_ZC);
+  int nxt[NEPT];
+  {
+    int a[NEPT];
     if (NDIM == 3) {
-      put(s2, nxt);
-      __syncthreads();
-      // three planes in flight per thread
-#pragma unroll
-      for (int e = 0; e < 2; e++) {
-        nxt[e] = nx2[e];
-        nx2[e] = nx3[e];
-      }
-      if (z + 3 < ze) fetch(z + 4, nx3);
+      fetch(zb - 1, a);
+      put(0, a);
+      fetch(zb, a);
+      put(1, a);
+      fetch(zb + 1, a);
+      put(2, a);
+      fetch(zb + 2, nxt);
     } else {
-      __syncthreads();
+      fetch(0, a);
+      put(0, a);
     }
-    const int *pm = pl[NDIM == 2 ? 0 : r3];
+  }
+  const int tx = threadIdx.x;
+  int sm = 0;  // ring slot of plane z-1
+  for (int z = zb; z < ze; z++) {
+    const int s1 = sm + 1 >= CP_RING ? sm + 1 - CP_RING : sm + 1;
+    const int s2 = s1 + 1 >= CP_RING ? s1 + 1 - CP_RING : s1 + 1;
+    const int s3 = s2 + 1 >= CP_RING ? s2 + 1 - CP_RING : s2 + 1;
+    if (NDIM == 3) {
+      // plane z+2 goes to a slot nobody reads this iteration; prefetch z+3
+      put(s3, nxt);
+      if (z + 3 < ze + 1) fetch(z + 3, nxt);
+    }
+    __syncthreads();
+    const int r3 = sm;
     const int *p0 = pl[NDIM == 2 ? 0 : s1];
+    const int *pm = pl[NDIM == 2 ? 0 : r3];
     const int *pp = pl[NDIM == 2 ? 0 : s2];
-    if (x < nx && y < ny) {
-      const int rv = p0[c];
-      const int64_t v = (int64_t)z * sxy + (int64_t)y * nx + x;
-      if (COUNTS) {
-        unsigned up = 0, valid = 0;
 #pragma unroll
-        for (int k = 0; k < K; k++) {
-          const int *P = St::dz(k) < 0 ? pm : (St::dz(k) > 0 ? pp : p0);
-          const int ru = P[c + St::dy(k) * CL_PX + St::dx(k)];
-          valid |= (unsigned)(ru >= 0) << k;
-          up |= (unsigned)(ru > rv) << k;
-        }
-        const unsigned lo = valid & ~up;
-        if (flags) flags[v] = (uint8_t)((up == 0 ? FL_MAX : 0) | (lo == 0 ? FL_MIN : 0));
-        lower[v] = (int16_t)__ldg(lut + lo);
-        upper[v] = (int16_t)__ldg(lut + up);
+    for (int ry = 0; ry < CP_RY; ry++) {
+    const int ty = threadIdx.y + ry * CP_TY;
+    const int x = x0 + 2 * tx, y = y0 + ty;
+    const int c = (ty + 1) * CP_PITCH + 2 * tx + 2;
+    if (y < ny && x < nx) {
+      // plane z rows y-1, y, y+1
+      const int2 c0 = *reinterpret_cast<const int2 *>(p0 + c);
+      const int a0m = p0[c - 1], a0p = p0[c + 2];
+      const int2 u0 = *reinterpret_cast<const int2 *>(p0 + c + CP_PITCH);
+      const int u0p = p0[c + CP_PITCH + 2];
+      const int2 d0 = *reinterpret_cast<const int2 *>(p0 + c - CP_PITCH);
+      const int d0m = p0[c - CP_PITCH - 1];
+      Nb2 A, B;
+      // reference offset order (triangulation.py:32-45)
+      A.v[0] = c0.y;  B.v[0] = a0p;            // (1,0,0)
+      A.v[1] = u0.x;  B.v[1] = u0.y;           // (0,1,0)
+      if (NDIM == 2) {
+        A.v[2] = u0.y;  B.v[2] = u0p;          // (1,1)
+        A.v[3] = a0m;   B.v[3] = c0.x;         // (-1,0)
+        A.v[4] = d0.x;  B.v[4] = d0.y;         // (0,-1)
+        A.v[5] = d0m;   B.v[5] = d0.x;         // (-1,-1)
       } else {
-        // invalid neighbours hold -1: never the signed max, always the
-        // unsigned max.  Packing (rank << 4 | k) keeps the arg of the extremum.
-        int hi = -1;
-        unsigned lo = 0xffffffffu;
+        const int2 cp = *reinterpret_cast<const int2 *>(pp + c);
+        const int cpp = pp[c + 2];
+        const int2 up = *reinterpret_cast<const int2 *>(pp + c + CP_PITCH);
+        const int upp = pp[c + CP_PITCH + 2];
+        const int2 cm = *reinterpret_cast<const int2 *>(pm + c);
+        const int cmm = pm[c - 1];
+        const int2 dm = *reinterpret_cast<const int2 *>(pm + c - CP_PITCH);
+        const int dmm = pm[c - CP_PITCH - 1];
+        A.v[2] = cp.x;   B.v[2] = cp.y;        // (0,0,1)
+        A.v[3] = u0.y;   B.v[3] = u0p;         // (1,1,0)
+        A.v[4] = cp.y;   B.v[4] = cpp;         // (1,0,1)
+        A.v[5] = up.x;   B.v[5] = up.y;        // (0,1,1)
+        A.v[6] = up.y;   B.v[6] = upp;         // (1,1,1)
+        A.v[7] = a0m;    B.v[7] = c0.x;        // (-1,0,0)
+        A.v[8] = d0.x;   B.v[8] = d0.y;        // (0,-1,0)
+        A.v[9] = cm.x;   B.v[9] = cm.y;        // (0,0,-1)
+        A.v[10] = d0m;   B.v[10] = d0.x;       // (-1,-1,0)
+        A.v[11] = cmm;   B.v[11] = cm.x;       // (-1,0,-1)
+        A.v[12] = dm.x;  B.v[12] = dm.y;       // (0,-1,-1)
+        A.v[13] = dmm;   B.v[13] = dm.x;       // (-1,-1,-1)
+      }
+      const int64_t vA = (int64_t)z * sxy + (int64_t)y * nx + x;
 #pragma unroll
-        for (int k = 0; k < K; k++) {
-          const int *P = St::dz(k) < 0 ? pm : (St::dz(k) > 0 ? pp : p0);
-          const int ru = P[c + St::dy(k) * CL_PX + St::dx(k)];
-          if (PTR == PTR_NONE) {
-            hi = max(hi, ru);
-            lo = min(lo, (unsigned)ru);
-          } else {
-            const int pk = (ru << 4) | k;  // ru < 2^27 (n < 2^27 for PTR kernels)
-            hi = max(hi, ru < 0 ? -1 : pk);
-            lo = min(lo, ru < 0 ? 0xffffffffu : (unsigned)pk);
+      for (int h = 0; h < 2; h++) {
+        const Nb2 &N = h == 0 ? A : B;
+        const int rv = h == 0 ? c0.x : c0.y;
+        const int64_t v = vA + h;
+        if (h == 1 && x + 1 >= nx) break;
+        if (COUNTS) {
+          unsigned upm = 0, valid = 0;
+#pragma unroll
+          for (int k = 0; k < K; k++) {
+            valid |= (unsigned)(N.v[k] >= 0) << k;
+            upm |= (unsigned)(N.v[k] > rv) << k;
+          }
+          const unsigned lo = valid & ~upm;
+          if (flags) flags[v] = (uint8_t)((upm == 0 ? FL_MAX : 0) | (lo == 0 ? FL_MIN : 0));
+          lower[v] = (int16_t)__ldg(lut + lo);
+          upper[v] = (int16_t)__ldg(lut + upm);
+        } else {
+          int hi = -1;
+          unsigned lo = 0xffffffffu;
+#pragma unroll
+          for (int k = 0; k < K; k += 2) {
+            int a = N.v[k], b = N.v[k + 1];
+            if (PTR != PTR_NONE) {  // ru < 2^27 (n <= 2^27)
+              a = a < 0 ? -1 : ((a << 4) | k);
+              b = b < 0 ? -1 : ((b << 4) | (k + 1));
+            }
+            hi = __vimax3_s32(hi, a, b);
+            lo = __vimin3_u32(lo, (unsigned)a, (unsigned)b);
+          }
+          const int hr = PTR == PTR_NONE ? hi : (hi < 0 ? -1 : (hi >> 4));
+          const unsigned lr = PTR == PTR_NONE ? lo : (lo == 0xffffffffu ? lo : (lo >> 4));
+          const bool ismax = hr < rv, ismin = lr > (unsigned)rv;
+          if (flags) flags[v] = (uint8_t)((ismax ? FL_MAX : 0) | (ismin ? FL_MIN : 0));
+          if (PTR != PTR_NONE) {
+            const bool self = PTR == PTR_ASC ? ismax : ismin;
+            const int kb = PTR == PTR_ASC ? (hi & 15) : (int)(lo & 15u);
+            int64_t d = 0;
+#pragma unroll
+            for (int k = 0; k < K; k++)
+              if (kb == k) d = St::dx(k) + (int64_t)nx * St::dy(k) + sxy * St::dz(k);
+            ptr[v] = (int)(self ? v : v + d);
           }
         }
-        const int hr = PTR == PTR_NONE ? hi : (hi < 0 ? -1 : (hi >> 4));
-        const unsigned lr = PTR == PTR_NONE ? lo : (lo == 0xffffffffu ? lo : (lo >> 4));
-        const bool ismax = hr < rv, ismin = lr > (unsigned)rv;
-        if (flags) flags[v] = (uint8_t)((ismax ? FL_MAX : 0) | (ismin ? FL_MIN : 0));
-        if (PTR != PTR_NONE) {
-          const bool self = PTR == PTR_ASC ? ismax : ismin;
-          const int kb = PTR == PTR_ASC ? (hi & 15) : (int)(lo & 15u);
-          int64_t d = 0;
-#pragma unroll
-          for (int k = 0; k < K; k++)
-            if (kb == k) d = St::dx(k) + (int64_t)nx * St::dy(k) + sxy * St::dz(k);
-          ptr[v] = (int)(self ? v : v + d);
-        }
       }
     }
-    r3 = s1;
-    __syncthreads();
+    }
+    sm = s1;
+    if (NDIM == 2) __syncthreads();
   }
 }
 
 inline void launch_classify(const Grid &g, const int32_t *rank, uint8_t *flags, int16_t *lower,
                             int16_t *upper, const uint8_t *lut, int32_t *ptr, int ptr_kind,
                             cudaStream_t s) {
-  dim3 blk(CL_TX, CL_TY);
-  dim3 grd((g.nx + CL_TX - 1) / CL_TX, (g.ny + CL_TY - 1) / CL_TY,
-           g.ndim == 2 ? 1 : (g.nz + CL_ZC - 1) / CL_ZC);
+  dim3 blk(CP_TX, CP_TY);
+  dim3 grd((g.nx + CP_W - 1) / CP_W, (g.ny + CP_TY * CP_RY - 1) / (CP_TY * CP_RY),
+           g.ndim == 2 ? 1 : (g.nz + CP_ZC - 1) / CP_ZC);
   bool counts = lower != nullptr;
 #define LTS_CL(ND, C, P) k_classify_tile<ND, C, P><<<grd, blk, 0, s>>>(g, rank, flags, lower, upper, lut, ptr)
   if (g.ndim == 2) {
