@@ -178,16 +178,15 @@ def main():
         return reference_arm(args)
 
     import torch
-    import torch.distributed as dist
     import paper_2009_00083_b200 as P
     from paper_2009_00083_b200 import _native as N
     from paper_2009_00083_b200 import synthetic as S
 
-    rank, world, local = dist_env()
+    from paper_2009_00083_b200 import replicas as R
+    rank, world, local = R.env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    R.init("nccl", dev)
 
     cfg = S.CONFIGS[args.config]
     f3d = S.make_field(args.config, args.seed)
@@ -220,8 +219,7 @@ def main():
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     launches0 = N.kernel_launches()
-    if world > 1:
-        dist.barrier()
+    R.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         for i in range(args.steps):
@@ -232,14 +230,10 @@ def main():
         torch.cuda.synchronize()
     launches = N.kernel_launches() - launches0
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    t_ms = sum(step_ms)
-    if world > 1:
-        tt = torch.tensor([t_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-        dist.barrier()
+    t_ms = R.max_over_ranks(sum(step_ms), dev)
+    R.barrier()
     ms_per_step = t_ms / args.steps
-    value = world * n / (ms_per_step / 1e3)
+    value = R.job_throughput(n, world, ms_per_step)
 
     # ---- phase breakdown (library CUDA events on the launching stream) ------
     flush.zero_()
@@ -315,12 +309,8 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         e_ms.append(a.elapsed_time(b))
-    e2e_t = sum(e_ms) / len(e_ms)
-    if world > 1:
-        tt = torch.tensor([e2e_t], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_t = float(tt.item())
-    e2e = {"value": world * n / (e2e_t / 1e3), "unit": UNIT,
+    e2e_t = R.max_over_ranks(sum(e_ms) / len(e_ms), dev)
+    e2e = {"value": R.job_throughput(n, world, e2e_t), "unit": UNIT,
            "h2d_bytes_per_step": 4 * n + 8 * (pm.size + pn.size), "d2h_bytes_per_step": 8 * n,
            "ms_per_step": e2e_t}
 
@@ -351,8 +341,7 @@ def main():
             "step_ms": step_ms,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    R.shutdown()
 
 
 if __name__ == "__main__":

@@ -77,3 +77,42 @@ def test_synthetic_generators_small():
     assert a.dtype == np.float32 and a.shape == (32, 32) and np.array_equal(a, b)
     assert S.cfg2(3, N=8).shape == (8, 8, 8)
     assert S.CONFIGS[3].dims == (256, 256, 256)
+
+
+def test_generators_match_full_size_digests():
+    """cfg1/cfg2 generators reproduce the fields the oracle digests were made
+    from (tests/golden/full_hashes.json)."""
+    import hashlib
+    import json
+    from paper_2009_00083_b200 import synthetic as S
+    data = json.load(open(os.path.join(ROOT, "tests", "golden", "full_hashes.json")))
+    for c in (1, 2):
+        f = S.make_field(c, 0).ravel()
+        assert hashlib.sha256(f.tobytes()).hexdigest() == data[str(c)]["f_sha"]
+
+
+def test_oracle_matches_full_size_cfg1_digest():
+    """The pinned CPU oracle reproduces its own full-size cfg1 digest."""
+    import hashlib
+    import json
+    from oracle import lts_oracle as O
+    from paper_2009_00083_b200 import synthetic as S
+    data = json.load(open(os.path.join(ROOT, "tests", "golden", "full_hashes.json")))["1"]
+    C = S.CONFIGS[1]
+    f = S.make_field(1, 0).ravel()
+    rank, _ = O.order_field(f)
+    mn, mx = O.extrema(C.dims, rank)
+    pm, pn = S.select_preserved(rank, mx, mn, C.n_keep_max, C.n_keep_min)
+    res = O.simplify(C.dims, f, pm, pn)
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    assert sha(res.G_rank.astype(np.int32)) == data["G_sha"]
+    assert sha(res.g) == data["g_sha"]
+
+
+def test_select_preserved_top_k():
+    from paper_2009_00083_b200 import synthetic as S
+    rank = np.array([5, 0, 3, 9, 1, 7, 2, 8, 4, 6])
+    mx = np.array([0, 3, 5, 7])
+    mn = np.array([1, 4, 6])
+    pm, pn = S.select_preserved(rank, mx, mn, 2, 1)
+    assert pm.tolist() == [3, 7] and pn.tolist() == [1]
