@@ -71,6 +71,9 @@ typedef struct {
   int64_t largest;     /* largest region size, saddle included                 */
   int64_t capped;      /* regions that hit the iteration cap (status 2)        */
   int64_t shared_saddles; /* regions whose saddle is shared with a sibling     */
+  int64_t maxima_edges;   /* edges of the maxima graph (discover)              */
+  int32_t boruvka_rounds; /* Boruvka rounds to settle every saddle level       */
+  int32_t big_regions;    /* regions handled by the CTA flood kernel           */
 } lts_pass_report_t;
 
 typedef struct {

@@ -39,7 +39,9 @@ class lts_options_t(ctypes.Structure):
 class lts_pass_report_t(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("n_iter_max", ctypes.c_int32), ("seeds", ctypes.c_int64),
                 ("regions", ctypes.c_int64), ("claimed", ctypes.c_int64), ("largest", ctypes.c_int64),
-                ("capped", ctypes.c_int64), ("shared_saddles", ctypes.c_int64)]
+                ("capped", ctypes.c_int64), ("shared_saddles", ctypes.c_int64),
+                ("maxima_edges", ctypes.c_int64), ("boruvka_rounds", ctypes.c_int32),
+                ("big_regions", ctypes.c_int32)]
 
 
 class lts_report_t(ctypes.Structure):

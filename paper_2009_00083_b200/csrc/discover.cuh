@@ -137,7 +137,21 @@ __global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ r
         if (!dup) bs[cnt++] = b;
       }
     }
-    int incl = cnt;
+    // warp-level de-duplication: lanes (consecutive vertices) that emit the
+    // same manifold pair keep only the heaviest edge (highest lower endpoint)
+    unsigned keep = 0;
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      const bool has = i < cnt;
+      if (__ballot_sync(0xffffffffu, has) == 0) break;
+      const unsigned long long key = has ? (((unsigned long long)(unsigned)a << 32) | (unsigned)bs[i]) : ~0ull;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int best = __reduce_max_sync(peers, has ? rv : -1);
+      // the lane holding the heaviest copy emits (ranks are distinct)
+      if (has && rv == best) keep |= 1u << i;
+    }
+    int kc = __popc(keep);
+    int incl = kc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -155,13 +169,14 @@ __global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ r
       s_base = acc ? atomicAdd(ecount, acc) : 0;
     }
     __syncthreads();
-    int slot = s_base + s_w[warp] + incl - cnt;
+    int slot = s_base + s_w[warp] + incl - kc;
 #pragma unroll
     for (int i = 0; i < K; i++)
-      if (i < cnt) {
-        ea[slot + i] = a;
-        eb[slot + i] = bs[i];
-        ew[slot + i] = rv;
+      if (keep >> i & 1u) {
+        ea[slot] = a;
+        eb[slot] = bs[i];
+        ew[slot] = rv;
+        slot++;
       }
     __syncthreads();
   }

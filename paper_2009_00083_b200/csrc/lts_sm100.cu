@@ -440,6 +440,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     LTS_KCHECK();
     LTS_TRY(readback(c, SC_ECOUNT, 1));
     const int ne = c.h_scal[SC_ECOUNT];
+    r.maxima_edges = ne;
     // Boruvka rounds: tau(m) = bottleneck to preserved maxima
     for (int round = 0; round < 64; round++) {
       k_bv_reset<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.best);
@@ -455,6 +456,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       LTS_KCHECK();
       LTS_TRY(readback(c, SC_ACTIVE, 2));
       if (c.h_scal[SC_ERR]) return lts_set_error(LTS_E_NO_SADDLE, "a discarded extremum cannot reach a preserved one");
+      r.boruvka_rounds = round + 1;
       if (c.h_scal[SC_ACTIVE] == 0) break;
     }
     // regions: union-find over edges between claimed endpoints
@@ -504,6 +506,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     g_launches++;
     LTS_TRY(readback(c, SC_NBIG, 1));
     const int nbig = c.h_scal[SC_NBIG];
+    r.big_regions = nbig;
     if (nbig > 0) {
       LTS_TRY(big_stream_fork(s));
       BigArgs B;

@@ -55,6 +55,9 @@ class PassReport:
     n_iter_max: int
     capped: int
     shared_saddles: int
+    maxima_edges: int = 0
+    boruvka_rounds: int = 0
+    big_regions: int = 0
 
 
 @dataclass
@@ -102,7 +105,8 @@ def _report(rep: "N.lts_report_t") -> SimplifyReport:
     for i in range(rep.n_passes):
         p = rep.passes[i]
         passes.append(PassReport("max" if p.kind == 0 else "min", p.seeds, p.regions, p.claimed,
-                                 p.largest, p.n_iter_max, p.capped, p.shared_saddles))
+                                 p.largest, p.n_iter_max, p.capped, p.shared_saddles,
+                                 p.maxima_edges, p.boruvka_rounds, p.big_regions))
     ph = {name: float(rep.phase_ms[i]) for i, name in enumerate(N.PHASES)}
     return SimplifyReport(
         ok=bool(rep.ok), outerIterations=int(rep.outer_iterations), restored=int(rep.restored),
@@ -224,7 +228,8 @@ def remove_pass(mesh: Triangulation, F: OrderField, preserve: ConstraintSet, kin
     torch.cuda.current_stream().synchronize()
     R, S = int(view.regions), int(view.slots)
     pr = PassReport(kind, rep.seeds, rep.regions, rep.claimed, rep.largest, rep.n_iter_max,
-                    rep.capped, rep.shared_saddles)
+                    rep.capped, rep.shared_saddles, rep.maxima_edges, rep.boruvka_rounds,
+                    rep.big_regions)
     return PassRegions(
         kind=kind,
         region_ptr=_view_tensor(ws, view.region_ptr, R + 1 if R else 0, torch.int64),
