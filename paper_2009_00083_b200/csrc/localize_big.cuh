@@ -31,6 +31,7 @@ constexpr int BIG_SMEM_WORDS = 10 * 1024;     // bit-set words in shared memory 
 constexpr int BIG_THRESHOLD = 1024;           // regions with k > this use this kernel
 
 struct BigArgs {
+  int *v0;           // per big region: first admissible boundary minimum
   int *inv;          // key -> local index, S + R entries (region base lo + rid)
   uint32_t *gbits;   // spill space for leaf / seen bit sets
   int *nrow;         // per slot: K local neighbour indices (-1 = not a member)
@@ -85,6 +86,20 @@ __device__ __forceinline__ void ct_update_warp(const CTree &T, int key, bool val
   }
 }
 
+// leaf-only frontier updates; the highest non-empty chunk (BIG_T leaf words)
+// is tracked with one warp-aggregated atomicMax per insertion batch
+__device__ __forceinline__ void leaf_remove(uint32_t *leaf, int key, bool valid) {
+  if (valid) atomicAnd(leaf + (key >> 5), ~(1u << (key & 31)));
+}
+
+__device__ __forceinline__ void leaf_insert(uint32_t *leaf, int *hi_chunk, int key, bool valid,
+                                            int chunk_shift) {
+  if (valid) atomicOr(leaf + (key >> 5), 1u << (key & 31));
+  const unsigned act = __activemask();
+  const int m = __reduce_max_sync(act, valid ? (key >> chunk_shift) : -1);
+  if (m >= 0 && (threadIdx.x & 31) == __ffs(act) - 1) atomicMax(hi_chunk, m);
+}
+
 // warp 0: the `need`-th largest key of F (need clamped to |F|).  Returns the
 // threshold key tau (-1 if F is empty) and the clamped need.
 __device__ __forceinline__ int ct_threshold(const CTree &T, int want, int &need_out) {
@@ -95,7 +110,7 @@ __device__ __forceinline__ int ct_threshold(const CTree &T, int want, int &need_
   for (;;) {
     int e = base + nel - 1 - lane;
     int c = 0;
-    if (lane < nel) c = l == 0 ? __popc(((volatile uint32_t *)T.leaf)[e]) : ((volatile int *)T.cnt[l])[e];
+    if (lane < nel) c = l == 0 ? __popc(T.leaf[e]) : T.cnt[l][e];
     int P = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -115,7 +130,7 @@ __device__ __forceinline__ int ct_threshold(const CTree &T, int want, int &need_
     int es = base + nel - 1 - src;
     need -= before;
     if (l == 0) {
-      uint32_t w = ((volatile uint32_t *)T.leaf)[es];
+      uint32_t w = T.leaf[es];
       // need-th highest set bit of w
       int b = 31;
       for (int r = 0;; b--) {
@@ -138,7 +153,7 @@ struct BigSmem {
   int pair_q[BIG_B * kMaxK];
   int pair_key[BIG_B * kMaxK];
   int wsum[BIG_T / 32 + 1];
-  int ncand, cut, nsrc, red, v0, qi, tau, carry;
+  int ncand, cut, nsrc, red, v0, qi, tau, carry, hi_chunk;
   CTree T;          // frontier descriptor (uniform; kept out of local memory)
   uint32_t *seen;   // bit set over local indices
   uint32_t bits[BIG_SMEM_WORDS];
@@ -154,7 +169,7 @@ struct BigRegion {
 };
 
 __device__ __forceinline__ bool seen_test(const uint32_t *seen, int q) {
-  return (((volatile const uint32_t *)seen)[q >> 5] >> (q & 31)) & 1u;
+  return (seen[q >> 5] >> (q & 31)) & 1u;
 }
 
 // desc floods map the sentinels +BIG -> k, -BIG -> 0; asc floods reverse
@@ -205,7 +220,10 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
   for (int l = 1; l <= T.top; l++)
     for (int i = tid; i < T.nb[l]; i += BIG_T) T.cnt[l][i] = 0;
   for (int i = tid; i < seen_words; i += BIG_T) seen[i] = 0u;
-  if (tid == 0) S.nsrc = 0;
+  if (tid == 0) {
+    S.nsrc = 0;
+    S.hi_chunk = -1;
+  }
   __syncthreads();
   for (int p = tid; p < k; p += BIG_T) G.inv[flood_key(cin[p], asc, k)] = p;
   // neighbour keys of this flood, one row per local index
@@ -213,19 +231,27 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     int q = G.row[i];
     G.rowkey[i] = q >= 0 ? flood_key(cin[q], asc, k) : -1;
   }
+  constexpr int CHUNK_SHIFT = 15;  // BIG_T leaf words = 32K keys per chunk
+  static_assert((32 * BIG_T) == (1 << CHUNK_SHIFT), "chunk = BIG_T leaf words");
   if (!asc) {
-    if (tid == 0) {
-      atomicOr(seen, 1u);
-      ct_insert(T, flood_key(cin[0], false, k));
-      S.nsrc = 1;
+    if (warp == 0) {
+      const bool src = lane == 0;
+      if (src) {
+        atomicOr(seen, 1u);
+        S.nsrc = 1;
+      }
+      leaf_insert(T.leaf, &S.hi_chunk, flood_key(cin[0], false, k), src, CHUNK_SHIFT);
     }
   } else {
-    for (int p = 1 + tid; p < k; p += BIG_T)
-      if ((G.sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) {
+    for (int p0 = 1; p0 < k; p0 += BIG_T) {
+      const int p = p0 + tid;
+      const bool src = p < k && (G.sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT);
+      if (src) {
         atomicOr(seen + (p >> 5), 1u << (p & 31));
-        ct_insert(T, flood_key(cin[p], true, k));
         atomicAdd(&S.nsrc, 1);
       }
+      leaf_insert(T.leaf, &S.hi_chunk, src ? flood_key(cin[p], true, k) : 0, src, CHUNK_SHIFT);
+    }
   }
   __syncthreads();
   if (S.nsrc == 0) {  // empty ascending flood keeps the previous labels
@@ -243,51 +269,40 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
   }
   for (;;) {
     BIG_TICK(8)
-    // (a) threshold: the Beff-th largest key of F (warp 0, counted descent)
-    if (warp == 0) {
-      int need = 0;
-      int tau = ct_threshold(T, Beff, need);
-      if (lane == 0) {
-        S.tau = tau;
-        S.ncand = need;
-        S.cut = need;
-      }
-    }
-    __syncthreads();
-    BIG_TICK(9)
-    const int nc = S.ncand;
-    if (nc == 0) break;
-    // enumerate keys >= tau in descending order: scan leaf words upward from
-    // tau's word; the rank from the bottom gives the output slot
+    // (a) candidates = the top Beff keys of F.  The CTA scans leaf words in
+    // chunks of BIG_T words (one word per thread, thread 0 = highest word),
+    // skipping empty chunks with the level-2 counts; a block scan of the
+    // popcounts gives every key its descending rank.
+    int nc = 0;
     {
-      const int tau = S.tau;
-      int carry = 0;
-      for (int w0 = tau >> 5; carry < nc && w0 < T.nw0; w0 += BIG_T) {
-        int w = w0 + tid;
-        uint32_t word = 0;
-        if (w < T.nw0) {
-          word = ((volatile uint32_t *)T.leaf)[w];
-          if (w == (tau >> 5)) word &= ~((1u << (tau & 31)) - 1u);  // keys >= tau
-        }
+      const int hi = S.hi_chunk;
+      int top_found = -1;
+      for (int ch = hi; ch >= 0 && nc < Beff; ch--) {
+        const int w = ch * BIG_T + (BIG_T - 1 - tid);
+        uint32_t word = w < T.nw0 ? T.leaf[w] : 0u;
         int tot;
-        int ex = big_scan_excl(__popc(word), S.wsum, tot);
-        int r = carry + ex;
-        while (word) {
-          int b = __ffs(word) - 1;
-          word &= word - 1;
-          int o = nc - 1 - r;
-          if (o >= 0) {
-            int key = (w << 5) + b;
-            S.cand_key[o] = key;
-            S.cand_p[o] = G.inv[key];
-            S.newmax[o] = -1;
-          }
-          r++;
+        int r = nc + big_scan_excl(__popc(word), S.wsum, tot);
+        while (word && r < Beff) {
+          int b = 31 - __clz(word);
+          word &= ~(1u << b);
+          S.cand_key[r++] = (w << 5) + b;
         }
-        carry += tot;
+        if (tot > 0 && top_found < 0) top_found = ch;
+        nc = min(Beff, nc + tot);
         __syncthreads();
       }
+      // chunks above the first non-empty one are empty: start lower next time
+      if (tid == 0) S.hi_chunk = top_found;
     }
+    BIG_TICK(9)
+    if (nc == 0) break;
+    if (tid == 0) S.cut = nc;
+    // local indices of the candidates: one independent load per thread
+    for (int i = tid; i < nc; i += BIG_T) {
+      S.cand_p[i] = G.inv[S.cand_key[i]];
+      S.newmax[i] = -1;
+    }
+    __syncthreads();
     BIG_TICK(10)
     // (b) exposure maxima of every candidate (row and key loads in parallel)
     for (int i = tid; i < nc * K; i += BIG_T) {
@@ -342,7 +357,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
       int i = i0 + tid;
       bool v = i < j;
       if (v) cout[S.cand_p[i]] = asc ? (e + i) : (k - 1 - (e + i));
-      ct_update_warp(T, v ? S.cand_key[i] : 0, v, -1);
+      leaf_remove(T.leaf, v ? S.cand_key[i] : 0, v);
     }
     BIG_TICK(13)
     for (int i0 = 0; i0 < j * K; i0 += BIG_T) {
@@ -353,7 +368,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
         uint32_t bit = 1u << (q & 31);
         ins = !(atomicOr(seen + (q >> 5), bit) & bit);
       }
-      ct_update_warp(T, ins ? S.pair_key[i] : 0, ins, 1);
+      leaf_insert(T.leaf, &S.hi_chunk, ins ? S.pair_key[i] : 0, ins, CHUNK_SHIFT);
     }
     e += j;
     if (dbg && tid == 0) {
@@ -433,6 +448,39 @@ __device__ bool big_states_equal(BigSmem &S, const int *a, const int *b, int k) 
   return r;
 }
 
+// Region adjacency rows, has_outside flags, identity initial order and v0 for
+// every large region, computed by the whole GPU before the flood kernel
+// (_kernels.py:453-481).  grid.y = big-region index, grid.x = slot chunks.
+template <int NDIM>
+__global__ void __launch_bounds__(256) k_big_rows(LocArgs A, BigArgs Bg) {
+  constexpr int K = NDIM == 2 ? 6 : 14;
+  const int qi = blockIdx.y;
+  const int rid = A.order[Bg.qbase + qi];
+  const int lo = A.rptr[rid];
+  const int k = A.rptr[rid + 1] - lo;
+  const int n = (int)A.g.n;
+  const int s = A.verts[lo];
+  const int srank = eff_rank(A.rank, s, A.rev, n);
+  int mine = 0x7fffffff;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < k; p += gridDim.x * blockDim.x) {
+    int x, y, z;
+    coords(A.g, A.verts[lo + p], x, y, z);
+    bool out = false;
+    int *row = Bg.nrow + ((size_t)lo + p) * K;
+#pragma unroll
+    for (int kk = 0; kk < K; kk++) {
+      int u = nbr_at(A.g, x, y, z, kk);
+      row[kk] = member(A, u, rid, s);
+      if (p >= 1 && u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) out = true;
+    }
+    A.sfl[lo + p] = out ? SF_OUT : 0;
+    if (out && p < mine) mine = p;
+    A.buf0[lo + p] = p;
+  }
+  mine = __reduce_min_sync(0xffffffffu, mine);
+  if ((threadIdx.x & 31) == 0 && mine != 0x7fffffff) atomicMin(Bg.v0 + qi, mine);
+}
+
 template <int NDIM>
 __global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
   constexpr int K = NDIM == 2 ? 6 : 14;
@@ -500,25 +548,8 @@ __global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
     __syncthreads();
     long long *dbg = (d_dbg_on && qi < DBG_MAX) ? d_dbg + qi * DBG_W : nullptr;
     long long c0 = clock64(), c1;
-    // rows, has_outside, v0 (_kernels.py:460-481)
-    if (tid == 0) S.v0 = 0x7fffffff;
-    __syncthreads();
-    const int srank = eff_rank(A.rank, G.s, A.rev, n);
-    for (int p = tid; p < k; p += BIG_T) {
-      int x, y, z;
-      coords(A.g, G.verts[p], x, y, z);
-      bool out = false;
-      int *row = Bg.nrow + ((size_t)lo + p) * K;
-#pragma unroll
-      for (int kk = 0; kk < K; kk++) {
-        int u = nbr_at(A.g, x, y, z, kk);
-        row[kk] = member(A, u, rid, G.s);
-        if (p >= 1 && u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) out = true;
-      }
-      G.sfl[p] = out ? SF_OUT : 0;
-      if (out) atomicMin(&S.v0, p);
-      b0[p] = p;
-    }
+    // rows, has_outside and v0 were produced by k_big_rows (grid-wide)
+    if (tid == 0) S.v0 = Bg.v0[qi];
     __syncthreads();
     const int v0 = S.v0;
     if (v0 == 0x7fffffff) {

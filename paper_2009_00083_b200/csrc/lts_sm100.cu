@@ -174,7 +174,7 @@ struct WS {
   int *verts, *buf0, *buf1, *buf2, *out;
   unsigned long long *gheap;
   uint8_t *sfl;
-  int *binv, *nrow, *nrowkey;
+  int *binv, *nrow, *nrowkey, *bigv0;
   uint32_t *gbits;
   rs::Bufs sb;
   int *bsum;
@@ -200,6 +200,7 @@ enum {
   SC_TMP = 28,
   SC_NBIG = 29,
   SC_BIGQ = 30,
+  SC_LARGEST = 31,
   SC_N = 64
 };
 
@@ -233,6 +234,7 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->gheap = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)s2);
   w->sfl = (uint8_t *)take((size_t)s2);
   w->binv = i32(3 * n + 8);
+  w->bigv0 = i32(n1);
   w->gbits = u32(6 * n + 64);
   w->nrow = i32((ndim == 2 ? 6 : 14) * s2);
   w->nrowkey = i32((ndim == 2 ? 6 : 14) * s2);
@@ -354,8 +356,12 @@ __global__ void k_loc_stats(const int *nit, const int *st, const int *rsize, int
   }
 }
 
+// out[0] = regions with k > th, out[2] = largest k (saddle included)
 __global__ void k_count_big(const int *rsize, int R, int th, int *out) {
-  GRID_STRIDE(r, R) if (rsize[r] + 1 > th) atomicAdd(out, 1);
+  GRID_STRIDE(r, R) {
+    if (rsize[r] + 1 > th) atomicAdd(out, 1);
+    atomicMax(out + 2, rsize[r] + 1);
+  }
 }
 
 static cudaStream_t g_side = nullptr;
@@ -504,14 +510,26 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     // to the CTA-batched flood on a side stream, the rest to warp floods
     k_count_big<<<NB(R), 256, 0, s>>>(w.rsize, R, BIG_THRESHOLD, w.scal + SC_NBIG);
     g_launches++;
-    LTS_TRY(readback(c, SC_NBIG, 1));
+    LTS_TRY(readback(c, SC_NBIG, 3));
     const int nbig = c.h_scal[SC_NBIG];
+    const int largest = c.h_scal[SC_LARGEST];
     r.big_regions = nbig;
     if (nbig > 0) {
       LTS_TRY(big_stream_fork(s));
       BigArgs B;
       B.inv = w.binv; B.gbits = w.gbits; B.nrow = w.nrow; B.nrowkey = w.nrowkey; B.qbase = 0; B.nbig = nbig;
       B.queue = w.scal + SC_BIGQ;
+      B.v0 = w.bigv0;
+      k_fill_int<<<NB(nbig), 256, 0, g_side>>>(w.bigv0, nbig, 0x7fffffff);
+      {
+        // slot chunks per region: enough blocks for the largest (first) one
+        int gx = (largest + 255) / 256;
+        if (gx > 256) gx = 256;
+        dim3 rg(gx, nbig);
+        if (c.g.ndim == 2) k_big_rows<2><<<rg, 256, 0, g_side>>>(A, B);
+        else k_big_rows<3><<<rg, 256, 0, g_side>>>(A, B);
+        g_launches += 2;
+      }
       int gb = nbig < 148 ? nbig : 148;
       if (c.g.ndim == 2) k_localize_big<2><<<gb, BIG_T, sizeof(BigSmem), g_side>>>(A, B);
       else k_localize_big<3><<<gb, BIG_T, sizeof(BigSmem), g_side>>>(A, B);
