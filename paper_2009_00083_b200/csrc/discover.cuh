@@ -369,13 +369,16 @@ __global__ void k_region_tops(const int *__restrict__ mlist, int nm, const uint8
 __global__ void k_region_label(const int *__restrict__ rank, int rev, int n,
                                const int *__restrict__ M, const uint8_t *__restrict__ vcls,
                                const int *__restrict__ acc, int *rpar, const int *__restrict__ ridx,
-                               int *reg_of, int *rsize) {
+                               int *reg_of, int *rsize, uint32_t *cbits) {
   GRID_STRIDE(v, n) {
     int m = M[v];
     int rid = -1;
     if (vcls[m] == 1 && eff_rank(rank, (int)v, rev, n) > acc[m]) rid = ridx[uf_find(rpar, m)];
     reg_of[v] = rid;
     unsigned act = __activemask();
+    // claimed bit set: warps cover 32 consecutive, 32-aligned vertices
+    unsigned cb = __ballot_sync(act, rid >= 0);
+    if ((threadIdx.x & 31) == __ffs(act) - 1) cbits[v >> 5] = cb;
     unsigned peers = __match_any_sync(act, rid);
     if (rid >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(rsize + rid, __popc(peers));
   }
@@ -383,21 +386,25 @@ __global__ void k_region_label(const int *__restrict__ rank, int rev, int n,
 
 // flag[t] = 1 if the vertex of effective rank t is claimed (for rank-ordered
 // compaction)
+__device__ __forceinline__ bool claimed_bit(const uint32_t *cbits, int v) {
+  return (__ldg(cbits + (v >> 5)) >> (v & 31)) & 1u;
+}
+
 __global__ void k_claimed_flags(const int *__restrict__ inv, int rev, int n,
-                                const int *__restrict__ reg_of, int *flag) {
+                                const uint32_t *__restrict__ cbits, int *flag) {
   GRID_STRIDE(t, n) {
     int v = inv[rev ? (n - 1 - t) : t];
-    flag[t] = reg_of[v] >= 0 ? 1 : 0;
+    flag[t] = claimed_bit(cbits, v) ? 1 : 0;
   }
 }
 
 __global__ void k_claimed_compact(const int *__restrict__ inv, int rev, int n,
-                                  const int *__restrict__ reg_of, const int *__restrict__ pos,
-                                  uint32_t *ckey, uint32_t *cval) {
+                                  const uint32_t *__restrict__ cbits, const int *__restrict__ reg_of,
+                                  const int *__restrict__ pos, uint32_t *ckey, uint32_t *cval) {
   GRID_STRIDE(t, n) {
     int v = inv[rev ? (n - 1 - t) : t];
-    int rid = reg_of[v];
-    if (rid >= 0) {
+    if (claimed_bit(cbits, v)) {
+      int rid = reg_of[v];
       int p = pos[t];
       ckey[p] = (uint32_t)rid;
       cval[p] = (uint32_t)v;

@@ -40,13 +40,15 @@ __device__ __forceinline__ void write_g(int v, int gp, int rev, int n, int *G, i
   Ginv[gr] = v;
 }
 
-__global__ void k_integrate_plain(const int *__restrict__ rank, int rev, int n,
-                                  const int *__restrict__ reg_of, const int *__restrict__ D,
+// rank order: inverse and prefix are read coalesced, the claimed test is a
+// bit-set probe, new inverses land in ascending (coalesced) order
+__global__ void k_integrate_plain(const int *__restrict__ inv, int rev, int n,
+                                  const uint32_t *__restrict__ cbits, const int *__restrict__ D,
                                   int *G, int *Ginv) {
-  GRID_STRIDE(v, n) {
-    if (reg_of[v] >= 0) continue;
-    int t = eff_rank(rank, (int)v, rev, n);
-    write_g((int)v, t + D[t], rev, n, G, Ginv);
+  GRID_STRIDE(t, n) {
+    int v = inv[rev ? (n - 1 - t) : t];
+    if ((__ldg(cbits + (v >> 5)) >> (v & 31)) & 1u) continue;
+    write_g(v, (int)t + D[t], rev, n, G, Ginv);
   }
 }
 

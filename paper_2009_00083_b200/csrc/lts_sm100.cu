@@ -175,6 +175,7 @@ struct WS {
   unsigned long long *gheap;
   uint8_t *sfl;
   int *binv, *nrow, *nrowkey, *bigv0;
+  uint32_t *cbits;
   uint32_t *gbits;
   rs::Bufs sb;
   int *bsum;
@@ -235,6 +236,7 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->sfl = (uint8_t *)take((size_t)s2);
   w->binv = i32(3 * n + 8);
   w->bigv0 = i32(n1);
+  w->cbits = u32(n / 32 + 64);
   w->gbits = u32(6 * n + 64);
   w->nrow = i32((ndim == 2 ? 6 : 14) * s2);
   w->nrowkey = i32((ndim == 2 ? 6 : 14) * s2);
@@ -470,7 +472,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     k_region_roots<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, w.acc, rank, rev, ni, w.rpar, w.ridx,
                                            w.scal + SC_NREG, w.rsad, w.rtop, w.rsize);
     k_region_tops<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, rank, rev, ni, w.rpar, w.ridx, w.rtop);
-    k_region_label<<<NB(n), 256, 0, s>>>(rank, rev, ni, w.M, w.vcls, w.acc, w.rpar, w.ridx, w.reg_of, w.rsize);
+    k_region_label<<<NB(n), 256, 0, s>>>(rank, rev, ni, w.M, w.vcls, w.acc, w.rpar, w.ridx, w.reg_of, w.rsize, w.cbits);
     g_launches += 4;
     LTS_KCHECK();
     LTS_TRY(readback(c, SC_NREG, 1));
@@ -481,14 +483,14 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     k_region_slots<<<NB(R), 256, 0, s>>>(w.rsize, R, w.rtmp);
     g_launches++;
     LTS_TRY(scan_int(w.rtmp, w.rptr, R, w.bsum, w.scal + SC_S, false, s));
-    k_claimed_flags<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.reg_of, w.flagscan);
+    k_claimed_flags<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.cbits, w.flagscan);
     g_launches++;
     LTS_TRY(scan_int(w.flagscan, w.flagscan, n, w.bsum, w.scal + SC_C, false, s));
     LTS_TRY(readback(c, SC_S, 2));
     S = c.h_scal[SC_S];
     C = c.h_scal[SC_C];
     LTS_CUDA(cudaMemcpyAsync(w.rptr + R, w.scal + SC_S, sizeof(int), cudaMemcpyDeviceToDevice, s));
-    k_claimed_compact<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.reg_of, w.flagscan, w.ckey, w.cval);
+    k_claimed_compact<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.cbits, w.reg_of, w.flagscan, w.ckey, w.cval);
     g_launches++;
     LTS_TRY(radix_sort(w.ckey, w.cval, C, bits_for(R - 1), false, w.skey, w.sval, nullptr, w.sb, s));
     k_place<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, w.loc_of);
@@ -573,7 +575,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       k_pos_of<<<NB(R), 256, 0, s>>>(w.oval, R, w.sib_rid, w.pos_of);
       g_launches++;
     }
-    k_integrate_plain<<<NB(n), 256, 0, s>>>(rank, rev, ni, w.reg_of, w.D, new_rank, new_inv);
+    k_integrate_plain<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.cbits, w.D, new_rank, new_inv);
     k_integrate_regions<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.out, w.rsad, w.rsize, w.rtop,
                                               w.delta, w.D, w.sib_rid, w.pos_of, R, nshared, rev, ni,
                                               new_rank, new_inv);
