@@ -28,7 +28,7 @@ namespace lts {
 constexpr int BIG_T = 1024;
 constexpr int BIG_B = 256;                    // max candidates per step
 constexpr int BIG_SMEM_WORDS = 10 * 1024;     // bit-set words in shared memory (rest of the SM is L1)
-constexpr int BIG_THRESHOLD = 1024;           // regions with k > this use this kernel
+constexpr int BIG_THRESHOLD = 256;            // regions with k > this use this kernel
 
 struct BigArgs {
   int *v0;           // per big region: first admissible boundary minimum
