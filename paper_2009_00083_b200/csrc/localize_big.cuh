@@ -28,6 +28,8 @@ namespace lts {
 constexpr int BIG_T = 1024;
 constexpr int BIG_B = 256;                    // max candidates per step
 constexpr int BIG_SMEM_WORDS = 10 * 1024;     // bit-set words in shared memory (rest of the SM is L1)
+constexpr int BIG_XMAX = 512;                 // climb continuation list
+constexpr int BIG_HOPS = 16;                  // sequential hops per step
 constexpr int BIG_THRESHOLD = 256;            // regions with k > this use this kernel
 
 struct BigArgs {
@@ -154,6 +156,8 @@ struct BigSmem {
   int pair_key[BIG_B * kMaxK];
   int wsum[BIG_T / 32 + 1];
   int ncand, cut, nsrc, red, v0, qi, tau, carry, hi_chunk;
+  int xcnt, enew;           // climb continuation: exposures above the window
+  int xkey[BIG_XMAX], xp[BIG_XMAX];
   CTree T;          // frontier descriptor (uniform; kept out of local memory)
   uint32_t *seen;   // bit set over local indices
   uint32_t bits[BIG_SMEM_WORDS];
@@ -269,6 +273,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
   }
   for (;;) {
     BIG_TICK(8)
+    if (tid == 0) S.xcnt = 0;
     // (a) candidates = the top Beff keys of F.  The CTA scans leaf words in
     // chunks of BIG_T words (one word per thread, thread 0 = highest word),
     // skipping empty chunks with the level-2 counts; a block scan of the
@@ -360,6 +365,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
       leaf_remove(T.leaf, v ? S.cand_key[i] : 0, v);
     }
     BIG_TICK(13)
+    const int kappa = S.cand_key[nc - 1];  // every key of F above kappa is known
     for (int i0 = 0; i0 < j * K; i0 += BIG_T) {
       int i = i0 + tid;
       int q = i < j * K ? S.pair_q[i] : -1;
@@ -369,6 +375,13 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
         ins = !(atomicOr(seen + (q >> 5), bit) & bit);
       }
       leaf_insert(T.leaf, &S.hi_chunk, ins ? S.pair_key[i] : 0, ins, CHUNK_SHIFT);
+      if (ins && S.pair_key[i] > kappa) {
+        int x = atomicAdd(&S.xcnt, 1);
+        if (x < BIG_XMAX) {
+          S.xkey[x] = S.pair_key[i];
+          S.xp[x] = q;
+        }
+      }
     }
     e += j;
     if (dbg && tid == 0) {
@@ -380,6 +393,64 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     else if (j * 4 < Beff && Beff > 8) Beff >>= 1;
     __syncthreads();
     BIG_TICK(14)
+    // (e) climb continuation (warp 0): while the largest known exposure beats
+    // the next candidate, it IS the next extraction; follow it with one row
+    // load per hop instead of a full CTA step.  Exposures above kappa join
+    // the known list; everything else stays in the bit set.
+    const int xc = S.xcnt;
+    if (j <= 4 && xc > 0 && xc <= BIG_XMAX) {  // block-uniform: climbs only
+      if (warp == 0) {
+        const int bound = j < nc ? S.cand_key[j] : kappa;
+        int m = xc, ee = e;
+        for (int hop = 0; hop < BIG_HOPS && m > 0; hop++) {
+          // argmax of the known list (keys are distinct)
+          int bk = -1;
+          for (int i = lane; i < m; i += 32) bk = max(bk, S.xkey[i]);
+          bk = __reduce_max_sync(0xffffffffu, bk);
+          if (bk <= bound) break;
+          int bi = 0x7fffffff;
+          for (int i = lane; i < m; i += 32)
+            if (S.xkey[i] == bk) bi = i;
+          bi = __reduce_min_sync(0xffffffffu, bi);
+          const int p = S.xp[bi];
+          __syncwarp();
+          if (lane == 0) {
+            cout[p] = asc ? ee : (k - 1 - ee);
+            S.xkey[bi] = S.xkey[m - 1];
+            S.xp[bi] = S.xp[m - 1];
+          }
+          leaf_remove(T.leaf, bk, lane == 0);
+          ee++;
+          m--;
+          __syncwarp();
+          int q = -1, key2 = -1;
+          if (lane < K) {
+            q = G.row[p * K + lane];
+            key2 = G.rowkey[p * K + lane];
+          }
+          bool ins = false;
+          if (q >= 0) {
+            uint32_t bit = 1u << (q & 31);
+            ins = !(atomicOr(seen + (q >> 5), bit) & bit);
+          }
+          leaf_insert(T.leaf, &S.hi_chunk, ins ? key2 : 0, ins, CHUNK_SHIFT);
+          const bool add = ins && key2 > kappa;
+          const unsigned am = __ballot_sync(0xffffffffu, add);
+          if (m + __popc(am) > BIG_XMAX) break;  // list full: leave the rest to the CTA
+          if (add) {
+            int x = m + __popc(am & lanemask_lt());
+            S.xkey[x] = key2;
+            S.xp[x] = q;
+          }
+          m += __popc(am);
+          __syncwarp();
+        }
+        if (lane == 0) S.enew = ee;
+      }
+      __syncthreads();
+      if (dbg && tid == 0) dbg[15] += S.enew - e;
+      e = S.enew;
+    }
   }
 #undef BIG_TICK
 }

@@ -26,6 +26,6 @@ out = out.reshape(256, 16)
 print("k steps cands committed flood_Mcyc check_Mcyc init_Mcyc nit")
 for r in out[:12]:
     print(r[0], r[1], r[2], r[3], round(r[4] / 1e6, 2), round(r[5] / 1e6, 2), round(r[6] / 1e6, 2), r[7],
-          "per-step cyc: gather %d fetch %d pairs %d cut %d commit %d insert %d loop %d" % tuple((r[8:15] / max(r[1], 1)).astype(int)), "threshold-only", int(r[15] / max(r[1], 1)))
+          "per-step cyc: gather %d fetch %d pairs %d cut %d commit %d insert %d loop %d" % tuple((r[8:15] / max(r[1], 1)).astype(int)), "climb-extractions", int(r[15]))
 nz = out[out[:, 0] > 0]
 print("regions", len(nz), "sum flood Mcyc", nz[:, 4].sum() / 1e6, "max", nz[:, 4].max() / 1e6)
