@@ -67,7 +67,7 @@ __global__ void k_roots(const int *__restrict__ ptr, int64_t n, int *root) {
 __global__ void k_mark_maxima(const uint8_t *__restrict__ flags, const uint8_t *__restrict__ pmark,
                               int kind, int64_t n, uint8_t *vcls, uint8_t *cst, int *mlist,
                               int *counts /* [0]=maxima [1]=D [2]=P */, int *comp, int *par,
-                              int *acc, int *rpar) {
+                              int *acc, int *rpar, unsigned long long *bestP) {
   GRID_STRIDE(v, n) {
     uint8_t fl = flags[v];
     bool ext = kind == 0 ? (fl & FL_MAX) : (fl & FL_MIN);
@@ -94,6 +94,66 @@ __global__ void k_mark_maxima(const uint8_t *__restrict__ flags, const uint8_t *
       par[v] = (int)v;
       acc[v] = 0x7fffffff;
       rpar[v] = (int)v;
+      bestP[v] = 0ull;
+    }
+  }
+}
+
+// Boruvka edge key: heavier first, ties by the other component id
+__device__ __forceinline__ unsigned long long bv_pack(int w, int c) {
+  return ((unsigned long long)(unsigned)(w + 1) << 32) | (unsigned)c;
+}
+
+// De-duplicating edge table: one slot per unordered manifold pair, holding the
+// heaviest weight (the only copy any bottleneck or region test can use).
+// Linear probing; keys are written once by CAS, weights by atomicMax.
+struct EdgeHash {
+  unsigned long long *key;  // ~0 = empty
+  int *w;                   // -1 = empty
+  int bits;                 // 0 = list mode (no table)
+  int *count, *overflow;
+};
+
+__device__ __forceinline__ void eh_insert(const EdgeHash &H, int a, int b, int w) {
+  const unsigned lo = (unsigned)min(a, b), hi = (unsigned)max(a, b);
+  const unsigned long long key = ((unsigned long long)lo << 32) | hi;
+  const unsigned long long mask = (1ull << H.bits) - 1;
+  unsigned long long h = (key * 0x9E3779B97F4A7C15ull) >> (64 - H.bits);
+  for (int probe = 0; probe < 64; probe++, h = (h + 1) & mask) {
+    unsigned long long k = *(volatile unsigned long long *)(H.key + h);
+    if (k == ~0ull) {
+      k = atomicCAS(H.key + h, ~0ull, key);
+      if (k == ~0ull) {
+        if (atomicAdd(H.count, 1) >= (1 << (H.bits - 1))) atomicOr(H.overflow, 1);
+        k = key;
+      }
+    }
+    if (k == key) {
+      if (*(volatile int *)(H.w + h) < w) atomicMax(H.w + h, w);
+      return;
+    }
+  }
+  atomicOr(H.overflow, 1);
+}
+
+// table -> edge list (a < b); order is irrelevant to every consumer
+__global__ void k_hash_compact(EdgeHash H, int *ea, int *eb, int *ew, int *cnt) {
+  const int64_t hc = 1ll << H.bits;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < hc; i0 += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = i0 + threadIdx.x;
+    unsigned long long k = i < hc ? H.key[i] : ~0ull;
+    bool has = k != ~0ull;
+    unsigned bal = __ballot_sync(0xffffffffu, has);
+    if (!bal) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(cnt, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (has) {
+      int slot = base + __popc(bal & ((1u << lane) - 1));
+      ea[slot] = (int)(k >> 32);
+      eb[slot] = (int)(unsigned)(k & 0xffffffffull);
+      ew[slot] = H.w[i];
     }
   }
 }
@@ -107,7 +167,8 @@ template <int NDIM>
 __global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ rank, int rev,
                                                const int *__restrict__ M,
                                                const uint8_t *__restrict__ vcls, int *ea, int *eb,
-                                               int *ew, int *ecount) {
+                                               int *ew, int *ecount,
+                                               unsigned long long *bestP, EdgeHash H) {
   constexpr int K = NDIM == 2 ? 6 : 14;
   __shared__ int s_w[8];
   __shared__ int s_base;
@@ -147,9 +208,23 @@ __global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ r
       const unsigned long long key = has ? (((unsigned long long)(unsigned)a << 32) | (unsigned)bs[i]) : ~0ull;
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       const int best = __reduce_max_sync(peers, has ? rv : -1);
-      // the lane holding the heaviest copy emits (ranks are distinct)
-      if (has && rv == best) keep |= 1u << i;
+      // the lane holding the heaviest copy emits (ranks are distinct).  An
+      // edge between a discarded and a preserved manifold only ever matters
+      // as the discarded side's heaviest edge into preserved territory: it is
+      // folded into bestP[discarded] instead of being emitted.
+      if (has && rv == best) {
+        const bool pa = vcls[a] == 2, pb = vcls[bs[i]] == 2;
+        if (pa != pb) {
+          const int d = pa ? bs[i] : a, pm = pa ? a : bs[i];
+          atomicMax(bestP + d, bv_pack(rv, pm));
+        } else if (H.bits) {
+          eh_insert(H, a, bs[i], rv);
+        } else {
+          keep |= 1u << i;
+        }
+      }
     }
+    if (H.bits) continue;  // block-uniform
     int kc = __popc(keep);
     int incl = kc;
 #pragma unroll
@@ -184,9 +259,6 @@ __global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ r
 
 // ---- Boruvka rounds over the maxima graph --------------------------------
 
-__device__ __forceinline__ unsigned long long bv_pack(int w, int c) {
-  return ((unsigned long long)(unsigned)(w + 1) << 32) | (unsigned)c;
-}
 
 __global__ void k_bv_reset(const int *__restrict__ mlist, int nm, unsigned long long *best) {
   GRID_STRIDE(i, nm) best[mlist[i]] = 0ull;
@@ -195,6 +267,20 @@ __global__ void k_bv_reset(const int *__restrict__ mlist, int nm, unsigned long 
 // each thread scans a run of consecutive edges (edges are emitted per vertex,
 // so runs share endpoints) and only issues an atomic when its endpoint changes
 constexpr int BV_RUN = 8;
+// every active component starts a round from its members' heaviest edges
+// into preserved territory
+__global__ void k_bv_pmax(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
+                          const uint8_t *__restrict__ cst, const uint8_t *__restrict__ vcls,
+                          const unsigned long long *__restrict__ bestP, unsigned long long *best) {
+  GRID_STRIDE(i, nm) {
+    int m = mlist[i];
+    if (vcls[m] != 1) continue;
+    int c = comp[m];
+    unsigned long long b = bestP[m];
+    if (cst[c] == 0 && b) atomicMax(best + c, b);
+  }
+}
+
 __global__ void k_bv_best(const int *__restrict__ ea, const int *__restrict__ eb,
                           const int *__restrict__ ew, int ne, const int *__restrict__ comp,
                           const uint8_t *__restrict__ cst, unsigned long long *best) {

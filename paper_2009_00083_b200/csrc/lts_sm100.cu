@@ -12,6 +12,7 @@
 // handful of scalars (counts) per pass; all arrays stay in HBM.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -166,10 +167,11 @@ struct WS {
   int *rsize, *rtop, *rsad, *order, *nit, *st, *rtmp, *rptr, *sib_rid, *pos_of, *lost, *okey;
   uint32_t *oval, *okey2;
   int64_t *rptr64;
-  unsigned long long *best;
+  unsigned long long *best, *bestP;
   uint8_t *flags, *pmark, *vcls, *cst;
   int *ea, *eb, *ew;
   int64_t emax;
+  char *ebuf;  // 12 * emax bytes: list-mode ea/eb/ew, or hash table + unique list
   // slots (2n)
   int *verts, *buf0, *buf1, *buf2, *out;
   unsigned long long *gheap;
@@ -227,10 +229,12 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->lost = i32(n1); w->okey = i32(n1); w->oval = u32(n1); w->okey2 = u32(n1);
   w->rptr64 = (int64_t *)take(sizeof(int64_t) * (size_t)n1);
   w->best = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)n);
+  w->bestP = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)n);
   w->flags = (uint8_t *)take((size_t)n); w->pmark = (uint8_t *)take((size_t)n);
   w->vcls = (uint8_t *)take((size_t)n); w->cst = (uint8_t *)take((size_t)n);
   w->emax = (int64_t)KH * n;
-  w->ea = i32(w->emax); w->eb = i32(w->emax); w->ew = i32(w->emax);
+  w->ebuf = take(12 * (size_t)w->emax);
+  w->ea = (int *)w->ebuf; w->eb = w->ea + w->emax; w->ew = w->eb + w->emax;
   w->verts = i32(s2); w->buf0 = i32(s2); w->buf1 = i32(s2); w->buf2 = i32(s2); w->out = i32(s2);
   w->gheap = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)s2);
   w->sfl = (uint8_t *)take((size_t)s2);
@@ -422,7 +426,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     Phase ph(c, LTS_PH_DISCOVER);
     LTS_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(int) * SC_N, s));
     k_mark_maxima<<<NB(n), 256, 0, s>>>(w.flags, pmark, kind, n, w.vcls, w.cst, w.mlist,
-                                         w.scal + SC_COUNTS, w.comp, w.par, w.acc, w.rpar);
+                                         w.scal + SC_COUNTS, w.comp, w.par, w.acc, w.rpar, w.bestP);
     g_launches++;
     LTS_KCHECK();
     LTS_TRY(readback(c, SC_COUNTS, 3));
@@ -440,19 +444,49 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     k_compress<<<NB(n), 256, 0, s>>>(w.ptr, n);
     k_roots<<<NB(n), 256, 0, s>>>(w.ptr, n, w.M);
     g_launches += 3;
-    if (c.g.ndim == 2)
-      k_edges<2><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
-    else
-      k_edges<3><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, w.ea, w.eb, w.ew, w.scal + SC_ECOUNT);
     g_launches += 3;
-    LTS_KCHECK();
-    LTS_TRY(readback(c, SC_ECOUNT, 1));
+    // maxima-graph edges, de-duplicated per manifold pair in a hash table
+    // sized from the maxima count; list mode if the table would overflow
+    static const bool force_list = getenv("LTS_FORCE_EDGE_LIST") != nullptr;  // test hook
+    int hbits = 12;
+    while (hbits < 30 && (1ll << hbits) < 64ll * nm) hbits++;
+    while (hbits > 10 && 18ll << hbits > 12 * w.emax) hbits--;
+    EdgeHash H{(unsigned long long *)w.ebuf, (int *)(w.ebuf + (8ll << hbits)), hbits,
+               w.scal + SC_ECOUNT, w.scal + SC_ACTIVE};
+    int *ea = w.ea, *eb = w.eb, *ew = w.ew;
+    for (int mode = force_list ? 1 : 0; mode < 2; mode++) {
+      if (mode == 0) {
+        ea = (int *)(w.ebuf + (12ll << hbits));
+        eb = ea + (1ll << (hbits - 1));
+        ew = eb + (1ll << (hbits - 1));
+        LTS_CUDA(cudaMemsetAsync(w.ebuf, 0xff, 12ull << hbits, s));
+      } else {
+        H.bits = 0;
+        ea = w.ea; eb = w.eb; ew = w.ew;
+        LTS_CUDA(cudaMemsetAsync(w.scal + SC_ECOUNT, 0, sizeof(int) * 2, s));
+        LTS_CUDA(cudaMemsetAsync(w.bestP, 0, sizeof(unsigned long long) * n, s));
+      }
+      if (c.g.ndim == 2)
+        k_edges<2><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
+      else
+        k_edges<3><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
+      g_launches++;
+      if (mode == 0) {
+        k_hash_compact<<<NB(1ll << hbits), 256, 0, s>>>(H, ea, eb, ew, w.scal + SC_TMP);
+        g_launches++;
+      }
+      LTS_KCHECK();
+      LTS_TRY(readback(c, SC_ECOUNT, 2));
+      if (mode == 0 && c.h_scal[SC_ACTIVE] == 0) break;
+    }
     const int ne = c.h_scal[SC_ECOUNT];
     r.maxima_edges = ne;
     // Boruvka rounds: tau(m) = bottleneck to preserved maxima
     for (int round = 0; round < 64; round++) {
       k_bv_reset<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.best);
-      k_bv_best<<<NB(ne), 256, 0, s>>>(w.ea, w.eb, w.ew, ne, w.comp, w.cst, w.best);
+      k_bv_pmax<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.vcls, w.bestP, w.best);
+      g_launches++;
+      if (ne > 0) k_bv_best<<<NB(ne), 256, 0, s>>>(ea, eb, ew, ne, w.comp, w.cst, w.best);
       k_bv_hook<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.best, w.par, w.wc, w.scal + SC_ERR);
       k_bv_cycle<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par);
       k_bv_jump<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par);
@@ -468,7 +502,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       if (c.h_scal[SC_ACTIVE] == 0) break;
     }
     // regions: union-find over edges between claimed endpoints
-    k_region_union<<<NB(ne), 256, 0, s>>>(w.ea, w.eb, w.ew, ne, w.vcls, w.acc, w.rpar);
+    if (ne > 0) k_region_union<<<NB(ne), 256, 0, s>>>(ea, eb, ew, ne, w.vcls, w.acc, w.rpar);
     k_region_roots<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, w.acc, rank, rev, ni, w.rpar, w.ridx,
                                            w.scal + SC_NREG, w.rsad, w.rtop, w.rsize);
     k_region_tops<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, rank, rev, ni, w.rpar, w.ridx, w.rtop);

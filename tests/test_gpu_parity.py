@@ -179,3 +179,21 @@ def test_idempotence():
     g2, G2, rep2 = P.simplify_field(mesh, g.values.clone(), cs, order=G)
     assert rep2.ok and rep2.regionCount == 0
     assert torch.equal(g2.values, g.values)
+
+
+def test_edge_list_fallback_matches():
+    """The maxima-graph edge table falls back to an undeduplicated list when the
+    hash table would overflow; force that path (process-wide switch, so run it
+    in a child) and compare against the oracle."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import test_gpu_parity as T\n"
+        "for name in ['rand2d_300x200', 'rand3d_40x36x30', 'cfg3_96', 'cfg4_512']:\n"
+        "    T.test_simplify_vs_oracle(name)\n"
+        "print('ok')\n" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, LTS_FORCE_EDGE_LIST="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
