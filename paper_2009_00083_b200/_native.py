@@ -12,7 +12,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblts_sm100.so")
+LIB_PATH = os.environ.get("LTS_SM100_LIB") or os.path.join(HERE, "liblts_sm100.so")  # override: dev variants
 
 LTS_OK = 0
 E_FIELD_NONFINITE = 1

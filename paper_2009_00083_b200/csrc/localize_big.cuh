@@ -26,7 +26,10 @@
 namespace lts {
 
 constexpr int BIG_T = 1024;
-constexpr int BIG_B = 256;                    // max candidates per step
+#ifndef LTS_BIG_B
+#define LTS_BIG_B 256
+#endif
+constexpr int BIG_B = LTS_BIG_B;              // max candidates per step
 constexpr int BIG_SMEM_WORDS = 10 * 1024;     // bit-set words in shared memory (rest of the SM is L1)
 constexpr int BIG_XMAX = 512;                 // climb continuation list
 constexpr int BIG_HOPS = 16;                  // sequential hops per step
@@ -37,7 +40,7 @@ struct BigArgs {
   int *inv;          // key -> local index, S + R entries (region base lo + rid)
   uint32_t *gbits;   // spill space for leaf / seen bit sets
   int *nrow;         // per slot: K local neighbour indices (-1 = not a member)
-  int *nrowkey;      // per slot: K neighbour keys of the current flood
+  int *nrowkey;      // per key: K neighbour keys of the current flood (rows in key order)
   int qbase, nbig;   // regions order[qbase .. qbase+nbig)
   int *queue;
 };
@@ -150,24 +153,22 @@ __device__ __forceinline__ int ct_threshold(const CTree &T, int want, int &need_
 
 struct BigSmem {
   int cand_key[BIG_B];
-  int cand_p[BIG_B];
   int newmax[BIG_B];
-  int pair_q[BIG_B * kMaxK];
   int pair_key[BIG_B * kMaxK];
   int wsum[BIG_T / 32 + 1];
   int ncand, cut, nsrc, red, v0, qi, tau, carry, hi_chunk;
   int xcnt, enew;           // climb continuation: exposures above the window
-  int xkey[BIG_XMAX], xp[BIG_XMAX];
+  int xkey[BIG_XMAX];
   CTree T;          // frontier descriptor (uniform; kept out of local memory)
-  uint32_t *seen;   // bit set over local indices
+  uint32_t *seen;   // bit set over keys
   uint32_t bits[BIG_SMEM_WORDS];
 };
 
 struct BigRegion {
   int rid, lo, k, s;
   const int *verts;
-  const int *row;   // k*K local neighbour indices
-  int *rowkey;      // k*K neighbour keys of the current flood (-1: not a member)
+  const int *row;   // k*K local neighbour indices, by local index
+  int *krow;        // (k+1)*K neighbour keys of the current flood, by key (-1: not a member)
   uint8_t *sfl;
   int *inv;
 };
@@ -219,7 +220,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
   const int k = G.k;
   const CTree &T = S.T;
   uint32_t *const seen = S.seen;
-  const int seen_words = (k + 31) >> 5;
+  const int seen_words = T.nw0;
   for (int i = tid; i < T.nw0; i += BIG_T) T.leaf[i] = 0u;
   for (int l = 1; l <= T.top; l++)
     for (int i = tid; i < T.nb[l]; i += BIG_T) T.cnt[l][i] = 0;
@@ -230,31 +231,35 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
   }
   __syncthreads();
   for (int p = tid; p < k; p += BIG_T) G.inv[flood_key(cin[p], asc, k)] = p;
-  // neighbour keys of this flood, one row per local index
+  // neighbour keys of this flood, one row per KEY: the flood never needs a
+  // local index except to write its label
   for (int i = tid; i < k * K; i += BIG_T) {
-    int q = G.row[i];
-    G.rowkey[i] = q >= 0 ? flood_key(cin[q], asc, k) : -1;
+    const int p = i / K, kk = i - p * K;
+    const int q = G.row[i];
+    G.krow[flood_key(cin[p], asc, k) * K + kk] = q >= 0 ? flood_key(cin[q], asc, k) : -1;
   }
   constexpr int CHUNK_SHIFT = 15;  // BIG_T leaf words = 32K keys per chunk
   static_assert((32 * BIG_T) == (1 << CHUNK_SHIFT), "chunk = BIG_T leaf words");
   if (!asc) {
     if (warp == 0) {
       const bool src = lane == 0;
+      const int key = flood_key(cin[0], false, k);
       if (src) {
-        atomicOr(seen, 1u);
+        atomicOr(seen + (key >> 5), 1u << (key & 31));
         S.nsrc = 1;
       }
-      leaf_insert(T.leaf, &S.hi_chunk, flood_key(cin[0], false, k), src, CHUNK_SHIFT);
+      leaf_insert(T.leaf, &S.hi_chunk, key, src, CHUNK_SHIFT);
     }
   } else {
     for (int p0 = 1; p0 < k; p0 += BIG_T) {
       const int p = p0 + tid;
       const bool src = p < k && (G.sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT);
+      const int key = src ? flood_key(cin[p], true, k) : 0;
       if (src) {
-        atomicOr(seen + (p >> 5), 1u << (p & 31));
+        atomicOr(seen + (key >> 5), 1u << (key & 31));
         atomicAdd(&S.nsrc, 1);
       }
-      leaf_insert(T.leaf, &S.hi_chunk, src ? flood_key(cin[p], true, k) : 0, src, CHUNK_SHIFT);
+      leaf_insert(T.leaf, &S.hi_chunk, key, src, CHUNK_SHIFT);
     }
   }
   __syncthreads();
@@ -302,26 +307,34 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     BIG_TICK(9)
     if (nc == 0) break;
     if (tid == 0) S.cut = nc;
-    // local indices of the candidates: one independent load per thread
-    for (int i = tid; i < nc; i += BIG_T) {
-      S.cand_p[i] = G.inv[S.cand_key[i]];
-      S.newmax[i] = -1;
-    }
+    // the label slot of candidate tid, in flight until the commit (BIG_B <= BIG_T)
+    const int cand_p = tid < nc ? G.inv[S.cand_key[tid]] : 0;
+    if (tid < nc) S.newmax[tid] = -1;
     __syncthreads();
     BIG_TICK(10)
-    // (b) exposure maxima of every candidate (row and key loads in parallel)
-    for (int i = tid; i < nc * K; i += BIG_T) {
-      int c = i / K, kk = i - c * K;
-      int off = S.cand_p[c] * K + kk;
-      int q = G.row[off];
-      int key = G.rowkey[off];
-      if (q >= 0 && !seen_test(seen, q)) {
-        atomicMax(&S.newmax[c], key);
-      } else {
-        q = -1;
+    // (b) exposure maxima of every candidate: all row loads issued first
+    {
+      constexpr int PPT = (BIG_B * K + BIG_T - 1) / BIG_T;
+      int nk[PPT];
+#pragma unroll
+      for (int t = 0; t < PPT; t++) {
+        const int i = tid + t * BIG_T;
+        nk[t] = -1;
+        if (i < nc * K) {
+          const int c = i / K;
+          nk[t] = G.krow[S.cand_key[c] * K + (i - c * K)];
+        }
       }
-      S.pair_q[i] = q;
-      S.pair_key[i] = key;
+#pragma unroll
+      for (int t = 0; t < PPT; t++) {
+        const int i = tid + t * BIG_T;
+        if (i < nc * K) {
+          int q = nk[t];
+          if (q >= 0 && !seen_test(seen, q)) atomicMax(&S.newmax[i / K], q);
+          else q = -1;
+          S.pair_key[i] = q;
+        }
+      }
     }
     __syncthreads();
     BIG_TICK(11)
@@ -358,29 +371,25 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     BIG_TICK(12)
     const int j = S.cut;
     // (d) commit the prefix: labels, leave F; its exposures join F
-    for (int i0 = 0; i0 < j; i0 += BIG_T) {
-      int i = i0 + tid;
-      bool v = i < j;
-      if (v) cout[S.cand_p[i]] = asc ? (e + i) : (k - 1 - (e + i));
-      leaf_remove(T.leaf, v ? S.cand_key[i] : 0, v);
+    {
+      const bool v = tid < j;
+      if (v) cout[cand_p] = asc ? (e + tid) : (k - 1 - (e + tid));
+      leaf_remove(T.leaf, v ? S.cand_key[tid] : 0, v);
     }
     BIG_TICK(13)
     const int kappa = S.cand_key[nc - 1];  // every key of F above kappa is known
     for (int i0 = 0; i0 < j * K; i0 += BIG_T) {
       int i = i0 + tid;
-      int q = i < j * K ? S.pair_q[i] : -1;
+      int q = i < j * K ? S.pair_key[i] : -1;
       bool ins = false;
       if (q >= 0) {
         uint32_t bit = 1u << (q & 31);
         ins = !(atomicOr(seen + (q >> 5), bit) & bit);
       }
-      leaf_insert(T.leaf, &S.hi_chunk, ins ? S.pair_key[i] : 0, ins, CHUNK_SHIFT);
-      if (ins && S.pair_key[i] > kappa) {
+      leaf_insert(T.leaf, &S.hi_chunk, ins ? q : 0, ins, CHUNK_SHIFT);
+      if (ins && q > kappa) {
         int x = atomicAdd(&S.xcnt, 1);
-        if (x < BIG_XMAX) {
-          S.xkey[x] = S.pair_key[i];
-          S.xp[x] = q;
-        }
+        if (x < BIG_XMAX) S.xkey[x] = q;
       }
     }
     e += j;
@@ -412,36 +421,26 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
           for (int i = lane; i < m; i += 32)
             if (S.xkey[i] == bk) bi = i;
           bi = __reduce_min_sync(0xffffffffu, bi);
-          const int p = S.xp[bi];
+          const int key2 = lane < K ? G.krow[bk * K + lane] : -1;
           __syncwarp();
           if (lane == 0) {
-            cout[p] = asc ? ee : (k - 1 - ee);
+            cout[G.inv[bk]] = asc ? ee : (k - 1 - ee);
             S.xkey[bi] = S.xkey[m - 1];
-            S.xp[bi] = S.xp[m - 1];
           }
           leaf_remove(T.leaf, bk, lane == 0);
           ee++;
           m--;
           __syncwarp();
-          int q = -1, key2 = -1;
-          if (lane < K) {
-            q = G.row[p * K + lane];
-            key2 = G.rowkey[p * K + lane];
-          }
           bool ins = false;
-          if (q >= 0) {
-            uint32_t bit = 1u << (q & 31);
-            ins = !(atomicOr(seen + (q >> 5), bit) & bit);
+          if (key2 >= 0) {
+            uint32_t bit = 1u << (key2 & 31);
+            ins = !(atomicOr(seen + (key2 >> 5), bit) & bit);
           }
           leaf_insert(T.leaf, &S.hi_chunk, ins ? key2 : 0, ins, CHUNK_SHIFT);
           const bool add = ins && key2 > kappa;
           const unsigned am = __ballot_sync(0xffffffffu, add);
           if (m + __popc(am) > BIG_XMAX) break;  // list full: leave the rest to the CTA
-          if (add) {
-            int x = m + __popc(am & lanemask_lt());
-            S.xkey[x] = key2;
-            S.xp[x] = q;
-          }
+          if (add) S.xkey[m + __popc(am & lanemask_lt())] = key2;
           m += __popc(am);
           __syncwarp();
         }
@@ -573,7 +572,7 @@ __global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
     G.sfl = A.sfl + G.lo;
     G.inv = Bg.inv + G.lo + G.rid;
     G.row = Bg.nrow + (size_t)G.lo * K;
-    G.rowkey = Bg.nrowkey + (size_t)G.lo * K;
+    G.krow = Bg.nrowkey + ((size_t)G.lo + G.rid) * K;
     G.s = G.verts[0];
     const int k = G.k, rid = G.rid, lo = G.lo;
     int *const b0 = A.buf0 + lo, *const b1 = A.buf1 + lo, *const b2 = A.buf2 + lo;
@@ -591,7 +590,7 @@ __global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
       T.top = l;
       uint32_t *sp = S.bits;
       int used = 0;
-      const int seen_words = (k + 31) >> 5;
+      const int seen_words = T.nw0;
       uint32_t *gp = Bg.gbits + 3 * (((size_t)lo + rid + 31) >> 5) + 8 * (size_t)rid;
       int ncnt = 0;
       for (int i = 1; i <= T.top; i++) ncnt += T.nb[i];
