@@ -155,8 +155,10 @@ int lts_bench_kernels(const float *f, int ndim, const int64_t *dims, int reps, d
                       void *ws, size_t ws_bytes, void *stream);
 
 /* Diagnostics: enable (1) / read per-region counters of the large-region
- * flood kernel: out[i*8 + (k, steps, candidates, committed, flood cycles,
- * check cycles, init cycles, n_iters)] for the first nregions big regions. */
+ * flood kernel: out[i*24 + (k, steps, candidates, committed, flood cycles,
+ * check cycles, init cycles, n_iters, per-phase cycles 8..14, climb
+ * extractions, gather chunk iterations, gather scan / extract cycles, climb
+ * steps)] for the first nregions (<= 256) big regions. */
 int lts_debug_big_stats(int enable, int64_t *out, int nregions);
 
 /* Number of CUDA kernels this library launched since load (diagnostics). */

@@ -25,13 +25,17 @@
 
 namespace lts {
 
-constexpr int BIG_T = 1024;
+#ifndef LTS_BIG_T
+#define LTS_BIG_T 1024
+#endif
+constexpr int BIG_T = LTS_BIG_T;
 #ifndef LTS_BIG_B
 #define LTS_BIG_B 256
 #endif
 constexpr int BIG_B = LTS_BIG_B;              // max candidates per step
 constexpr int BIG_SMEM_WORDS = 10 * 1024;     // bit-set words in shared memory (rest of the SM is L1)
-constexpr int BIG_XMAX = 512;                 // climb continuation list
+constexpr int BIG_XMAX = 512;                 // climb continuation list (index fits 9 bits)
+static_assert(BIG_XMAX <= 512, "packed climb argmax");
 constexpr int BIG_HOPS = 16;                  // sequential hops per step
 constexpr int BIG_THRESHOLD = 256;            // regions with k > this use this kernel
 
@@ -48,7 +52,7 @@ struct BigArgs {
 // optional per-region instrumentation (lts_debug_big_stats): big-queue slot i
 // records [k, steps, candidates, committed, flood cycles, check cycles, init
 // cycles, n_iters]
-constexpr int DBG_MAX = 256, DBG_W = 16;
+constexpr int DBG_MAX = 256, DBG_W = 24;
 __device__ long long d_dbg[DBG_MAX * DBG_W];
 __device__ int d_dbg_on;
 
@@ -185,8 +189,9 @@ __device__ __forceinline__ int flood_key(int c, bool asc, int k) {
   return c;
 }
 
-// block-wide exclusive scan (BIG_T threads): warp scans, warp 0 scans the
-// warp totals, one extra barrier
+// block-wide exclusive scan (BIG_T threads) with one barrier: warp scans,
+// then every warp scans the warp totals itself.  The caller must barrier
+// before wsum is written again.
 __device__ __forceinline__ int big_scan_excl(int x, int *wsum, int &total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int inc = x;
@@ -197,20 +202,15 @@ __device__ __forceinline__ int big_scan_excl(int x, int *wsum, int &total) {
   }
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
-  if (warp == 0) {
-    int v = lane < BIG_T / 32 ? wsum[lane] : 0;
-    int p = v;
+  const int v = lane < BIG_T / 32 ? wsum[lane] : 0;
+  int p = v;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, p, o);
-      if (lane >= o) p += y;
-    }
-    if (lane < BIG_T / 32) wsum[lane] = p - v;
-    if (lane == 31) wsum[BIG_T / 32] = p;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, p, o);
+    if (lane >= o) p += y;
   }
-  __syncthreads();
-  total = wsum[BIG_T / 32];
-  return wsum[warp] + inc - x;
+  total = __shfl_sync(0xffffffffu, p, 31);
+  return __shfl_sync(0xffffffffu, p - v, warp) + inc - x;
 }
 
 template <int K>
@@ -230,20 +230,21 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     S.hi_chunk = -1;
   }
   __syncthreads();
-  for (int p = tid; p < k; p += BIG_T) G.inv[flood_key(cin[p], asc, k)] = p;
+  auto key_of = [&](int p) -> int { return flood_key(cin[p], asc, k); };
+  for (int p = tid; p < k; p += BIG_T) G.inv[key_of(p)] = p;
   // neighbour keys of this flood, one row per KEY: the flood never needs a
   // local index except to write its label
   for (int i = tid; i < k * K; i += BIG_T) {
     const int p = i / K, kk = i - p * K;
     const int q = G.row[i];
-    G.krow[flood_key(cin[p], asc, k) * K + kk] = q >= 0 ? flood_key(cin[q], asc, k) : -1;
+    G.krow[key_of(p) * K + kk] = q >= 0 ? key_of(q) : -1;
   }
-  constexpr int CHUNK_SHIFT = 15;  // BIG_T leaf words = 32K keys per chunk
+  constexpr int CHUNK_SHIFT = BIG_T == 1024 ? 15 : BIG_T == 512 ? 14 : 13;  // BIG_T leaf words per chunk
   static_assert((32 * BIG_T) == (1 << CHUNK_SHIFT), "chunk = BIG_T leaf words");
   if (!asc) {
     if (warp == 0) {
       const bool src = lane == 0;
-      const int key = flood_key(cin[0], false, k);
+      const int key = key_of(0);
       if (src) {
         atomicOr(seen + (key >> 5), 1u << (key & 31));
         S.nsrc = 1;
@@ -254,7 +255,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     for (int p0 = 1; p0 < k; p0 += BIG_T) {
       const int p = p0 + tid;
       const bool src = p < k && (G.sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT);
-      const int key = src ? flood_key(cin[p], true, k) : 0;
+      const int key = src ? key_of(p) : 0;
       if (src) {
         atomicOr(seen + (key >> 5), 1u << (key & 31));
         atomicAdd(&S.nsrc, 1);
@@ -269,6 +270,11 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     return;
   }
   int e = 0;
+  // instrumentation accumulates in registers (a global += per tick would
+  // stall thread 0 on a load and perturb the barriers being measured)
+  long long tacc[DBG_W];
+#pragma unroll
+  for (int i = 0; i < DBG_W; i++) tacc[i] = 0;
   long long tq = clock64(), tn;
 #define BIG_TICK(slot)                          \
   if (dbg && tid == 0) {                        \
@@ -292,14 +298,26 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
         uint32_t word = w < T.nw0 ? T.leaf[w] : 0u;
         int tot;
         int r = nc + big_scan_excl(__popc(word), S.wsum, tot);
+        if (dbg && tid == 0) {
+          tn = clock64();
+          tacc[16] += 1;
+          tacc[17] += tn - tq;
+          tq = tn;
+        }
         while (word && r < Beff) {
           int b = 31 - __clz(word);
           word &= ~(1u << b);
+          S.newmax[r] = -1;
           S.cand_key[r++] = (w << 5) + b;
         }
         if (tot > 0 && top_found < 0) top_found = ch;
         nc = min(Beff, nc + tot);
         __syncthreads();
+        if (dbg && tid == 0) {
+          tn = clock64();
+          tacc[18] += tn - tq;
+          tq = tn;
+        }
       }
       // chunks above the first non-empty one are empty: start lower next time
       if (tid == 0) S.hi_chunk = top_found;
@@ -309,8 +327,6 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     if (tid == 0) S.cut = nc;
     // the label slot of candidate tid, in flight until the commit (BIG_B <= BIG_T)
     const int cand_p = tid < nc ? G.inv[S.cand_key[tid]] : 0;
-    if (tid < nc) S.newmax[tid] = -1;
-    __syncthreads();
     BIG_TICK(10)
     // (b) exposure maxima of every candidate: all row loads issued first
     {
@@ -394,9 +410,9 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     }
     e += j;
     if (dbg && tid == 0) {
-      dbg[1] += 1;
-      dbg[2] += nc;
-      dbg[3] += j;
+      tacc[1] += 1;
+      tacc[2] += nc;
+      tacc[3] += j;
     }
     if (j == nc && nc == Beff && Beff < BIG_B) Beff *= 2;
     else if (j * 4 < Beff && Beff > 8) Beff >>= 1;
@@ -408,19 +424,28 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     // the known list; everything else stays in the bit set.
     const int xc = S.xcnt;
     if (j <= 4 && xc > 0 && xc <= BIG_XMAX) {  // block-uniform: climbs only
+      if (dbg && tid == 0) tacc[19] += 1;
       if (warp == 0) {
         const int bound = j < nc ? S.cand_key[j] : kappa;
         int m = xc, ee = e;
         for (int hop = 0; hop < BIG_HOPS && m > 0; hop++) {
-          // argmax of the known list (keys are distinct)
-          int bk = -1;
-          for (int i = lane; i < m; i += 32) bk = max(bk, S.xkey[i]);
-          bk = __reduce_max_sync(0xffffffffu, bk);
+          // argmax of the known list (keys are distinct): one packed
+          // (key, index) reduction when keys fit in 23 bits
+          int bk = -1, bi = 0x7fffffff;
+          if (k < (1 << 22)) {
+            unsigned pk = 0u;
+            for (int i = lane; i < m; i += 32) pk = max(pk, ((unsigned)(S.xkey[i] + 1) << 9) | (unsigned)i);
+            pk = __reduce_max_sync(0xffffffffu, pk);
+            bk = (int)(pk >> 9) - 1;
+            bi = (int)(pk & 511u);
+          } else {
+            for (int i = lane; i < m; i += 32) bk = max(bk, S.xkey[i]);
+            bk = __reduce_max_sync(0xffffffffu, bk);
+            for (int i = lane; i < m; i += 32)
+              if (S.xkey[i] == bk) bi = i;
+            bi = __reduce_min_sync(0xffffffffu, bi);
+          }
           if (bk <= bound) break;
-          int bi = 0x7fffffff;
-          for (int i = lane; i < m; i += 32)
-            if (S.xkey[i] == bk) bi = i;
-          bi = __reduce_min_sync(0xffffffffu, bi);
           const int key2 = lane < K ? G.krow[bk * K + lane] : -1;
           __syncwarp();
           if (lane == 0) {
@@ -447,11 +472,16 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
         if (lane == 0) S.enew = ee;
       }
       __syncthreads();
-      if (dbg && tid == 0) dbg[15] += S.enew - e;
+      if (dbg && tid == 0) tacc[15] += S.enew - e;
       e = S.enew;
     }
   }
 #undef BIG_TICK
+  if (dbg && tid == 0) {
+#pragma unroll
+    for (int i = 1; i < DBG_W; i++)
+      if (i < 4 || i > 7) dbg[i] += tacc[i];
+  }
 }
 
 // after a descending flood: SF_MIN marks, true if an unauthorized minimum
@@ -616,10 +646,11 @@ __global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
       S.seen = (used + seen_words <= BIG_SMEM_WORDS) ? sp : gp;
     }
     __syncthreads();
-    long long *dbg = (d_dbg_on && qi < DBG_MAX) ? d_dbg + qi * DBG_W : nullptr;
+    const int qa = Bg.qbase + qi;  // absolute big-queue position
+    long long *dbg = (d_dbg_on && qa < DBG_MAX) ? d_dbg + qa * DBG_W : nullptr;
     long long c0 = clock64(), c1;
     // rows, has_outside and v0 were produced by k_big_rows (grid-wide)
-    if (tid == 0) S.v0 = Bg.v0[qi];
+    if (tid == 0) S.v0 = Bg.v0[qa];
     __syncthreads();
     const int v0 = S.v0;
     if (v0 == 0x7fffffff) {

@@ -363,6 +363,7 @@ __global__ void k_loc_stats(const int *nit, const int *st, const int *rsize, int
 }
 
 // out[0] = regions with k > th, out[2] = largest k (saddle included)
+// out[0] = #regions with k > th, out[2] = largest k
 __global__ void k_count_big(const int *rsize, int R, int th, int *out) {
   GRID_STRIDE(r, R) {
     if (rsize[r] + 1 > th) atomicAdd(out, 1);

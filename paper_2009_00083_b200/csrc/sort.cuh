@@ -106,8 +106,11 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t *war
 __device__ long long d_sort_dbg[8];
 __device__ int d_sort_dbg_on;
 
+#ifndef LTS_OS_MINB
+#define LTS_OS_MINB 1
+#endif
 template <bool FLOATKEY, bool HAS_VALS, bool WRITE_KEYS, bool WRITE_RANK>
-__global__ void __launch_bounds__(THREADS) k_onesweep(
+__global__ void __launch_bounds__(THREADS, LTS_OS_MINB) k_onesweep(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int32_t *__restrict__ rank_out, int64_t n, int shift,
     const uint32_t *__restrict__ offs, uint32_t *status, uint32_t *tile_ctr) {
