@@ -22,6 +22,7 @@
 // Parity with the reference sweep is checked in tests/test_gpu_parity.py.
 #pragma once
 #include "lts_common.cuh"
+#include "classify.cuh"  // Stencil
 
 namespace lts {
 
@@ -255,6 +256,173 @@ __global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ r
       }
     __syncthreads();
   }
+}
+
+// Tiled form of k_edges.  A CTA owns a 32 x 8 (x, y) column of the grid and
+// marches in z (one z plane for 2D grids); the manifold labels M and the
+// ranks of planes z-1..z+1 sit in a 5-slot shared-memory ring with halo, so
+// the 14-neighbour tests never touch L1/L2.  Edges found by the CTA are
+// combined in a shared hash table (one slot per manifold pair, heaviest
+// weight) and flushed to the global table / bestP once it fills and at the
+// end: a manifold boundary crossing the tile costs one global update instead
+// of one per boundary vertex.
+constexpr int ET_TX = 32, ET_TY = 8, ET_ZC = 16, ET_RING = 5;
+constexpr int ET_PX = ET_TX + 2, ET_PY = ET_TY + 2, ET_PL = ET_PX * ET_PY;
+constexpr int ET_NT = ET_TX * ET_TY, ET_NEPT = (ET_PL + ET_NT - 1) / ET_NT;
+constexpr int ET_HT = 2048, ET_FLUSH = 1024;  // shared table slots / flush level
+
+__device__ __forceinline__ void edge_global(const EdgeHash &H, const uint8_t *__restrict__ vcls,
+                                            unsigned long long *bestP, int *ea, int *eb, int *ew,
+                                            int *ecount, int a, int b, int w) {
+  const bool pa = vcls[a] == 2, pb = vcls[b] == 2;
+  if (pa && pb) return;  // preserved-preserved: never needed
+  if (pa != pb) {
+    const int d = pa ? b : a, pm = pa ? a : b;
+    atomicMax(bestP + d, bv_pack(w, pm));
+  } else if (H.bits) {
+    eh_insert(H, a, b, w);
+  } else {
+    const int slot = atomicAdd(ecount, 1);
+    ea[slot] = a;
+    eb[slot] = b;
+    ew[slot] = w;
+  }
+}
+
+template <int NDIM>
+__global__ void __launch_bounds__(ET_NT) k_edges_tile(Grid g, const int *__restrict__ rank, int rev,
+                                                    const int *__restrict__ M,
+                                                    const uint8_t *__restrict__ vcls, int *ea, int *eb,
+                                                    int *ew, int *ecount, unsigned long long *bestP,
+                                                    EdgeHash H) {
+  using St = Stencil<NDIM>;
+  constexpr int K = St::K;
+  constexpr int NP = NDIM == 2 ? 1 : ET_RING;
+  __shared__ int sM[NP][ET_PL], sR[NP][ET_PL];
+  __shared__ unsigned long long hkey[ET_HT];
+  __shared__ int hw[ET_HT];
+  __shared__ int hcount;
+  const int tid = threadIdx.y * ET_TX + threadIdx.x;
+  const int x0 = blockIdx.x * ET_TX, y0 = blockIdx.y * ET_TY;
+  const int nx = g.nx, ny = g.ny, nz = g.nz, n = (int)g.n;
+  const int64_t sxy = (int64_t)nx * ny;
+  for (int i = tid; i < ET_HT; i += ET_NT) {
+    hkey[i] = ~0ull;
+    hw[i] = -1;
+  }
+  if (tid == 0) hcount = 0;
+  // rank planes hold effective ranks (rev applied); -1 / M = -1 outside
+  auto fetch = [&](int z, int *rm, int *rr) {
+#pragma unroll
+    for (int e = 0; e < ET_NEPT; e++) {
+      const int i = tid + e * ET_NT;
+      const int py = i / ET_PX, px = i - py * ET_PX;
+      const int gx = x0 + px - 1, gy = y0 + py - 1;
+      const bool in = i < ET_PL && z >= 0 && z < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+      const int64_t gv = (int64_t)z * sxy + (int64_t)gy * nx + gx;
+      rm[e] = in ? __ldg(M + gv) : -1;
+      const int r = in ? __ldg(rank + gv) : 0;
+      rr[e] = rev ? n - 1 - r : r;
+    }
+  };
+  auto put = [&](int slot, const int *rm, const int *rr) {
+#pragma unroll
+    for (int e = 0; e < ET_NEPT; e++) {
+      const int i = tid + e * ET_NT;
+      if (i < ET_PL) {
+        sM[slot][i] = rm[e];
+        sR[slot][i] = rr[e];
+      }
+    }
+  };
+  auto flush = [&]() {
+    __syncthreads();
+    for (int i = tid; i < ET_HT; i += ET_NT) {
+      const unsigned long long kk = hkey[i];
+      if (kk != ~0ull) {
+        edge_global(H, vcls, bestP, ea, eb, ew, ecount, (int)(kk >> 32), (int)(unsigned)(kk & 0xffffffffu), hw[i]);
+        hkey[i] = ~0ull;
+        hw[i] = -1;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) hcount = 0;
+    __syncthreads();
+  };
+  const int zb = NDIM == 2 ? 0 : blockIdx.z * ET_ZC;
+  const int ze = NDIM == 2 ? 1 : min(nz, zb + ET_ZC);
+  int nm[ET_NEPT], nr[ET_NEPT];
+  {
+    int am[ET_NEPT], ar[ET_NEPT];
+    if (NDIM == 3) {
+      fetch(zb - 1, am, ar);
+      put(0, am, ar);
+      fetch(zb, am, ar);
+      put(1, am, ar);
+      fetch(zb + 1, am, ar);
+      put(2, am, ar);
+      fetch(zb + 2, nm, nr);
+    } else {
+      fetch(0, am, ar);
+      put(0, am, ar);
+    }
+  }
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  const int c = (threadIdx.y + 1) * ET_PX + threadIdx.x + 1;
+  int sm = 0;
+  for (int z = zb; z < ze; z++) {
+    const int s1 = sm + 1 >= ET_RING ? sm + 1 - ET_RING : sm + 1;
+    const int s2 = s1 + 1 >= ET_RING ? s1 + 1 - ET_RING : s1 + 1;
+    const int s3 = s2 + 1 >= ET_RING ? s2 + 1 - ET_RING : s2 + 1;
+    if (NDIM == 3) {
+      put(s3, nm, nr);
+      if (z + 3 < ze + 1) fetch(z + 3, nm, nr);
+    }
+    // one barrier per plane; it also carries the (uniform) flush decision
+    if (__syncthreads_or(tid == 0 && hcount > ET_FLUSH)) flush();
+    const int *m0 = sM[NDIM == 2 ? 0 : s1], *mm = sM[NDIM == 2 ? 0 : sm], *mp = sM[NDIM == 2 ? 0 : s2];
+    const int *r0 = sR[NDIM == 2 ? 0 : s1], *rm_ = sR[NDIM == 2 ? 0 : sm], *rp = sR[NDIM == 2 ? 0 : s2];
+    if (x < nx && y < ny) {
+      const int a = m0[c], rv = r0[c];
+      int d0 = -1, d1 = -1, d2 = -1;  // manifolds this vertex already sent
+#pragma unroll
+      for (int k = 0; k < K; k++) {
+        const int dz = St::dz(k);
+        const int o = c + St::dx(k) + ET_PX * St::dy(k);
+        const int *mk = dz == 0 ? m0 : (dz > 0 ? mp : mm);
+        const int *rk = dz == 0 ? r0 : (dz > 0 ? rp : rm_);
+        const int b = mk[o];
+        if (b == a || b < 0) continue;
+        if (rk[o] < rv) continue;                      // owned by the lower endpoint
+        if (b == d0 || b == d1 || b == d2) continue;  // same weight rv: a duplicate
+        d2 = d1;
+        d1 = d0;
+        d0 = b;
+        // shared table: one slot per unordered manifold pair, max weight
+        const unsigned lo = (unsigned)min(a, b), hi = (unsigned)max(a, b);
+        const unsigned long long key = ((unsigned long long)lo << 32) | hi;
+        unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 53) & (ET_HT - 1);
+        bool done = false;
+        for (int probe = 0; probe < 32 && !done; probe++, h = (h + 1) & (ET_HT - 1)) {
+          unsigned long long kk = hkey[h];
+          if (kk == ~0ull) {
+            kk = atomicCAS(hkey + h, ~0ull, key);
+            if (kk == ~0ull) {
+              atomicAdd(&hcount, 1);
+              kk = key;
+            }
+          }
+          if (kk == key) {
+            if (hw[h] < rv) atomicMax(hw + h, rv);
+            done = true;
+          }
+        }
+        if (!done) edge_global(H, vcls, bestP, ea, eb, ew, ecount, (int)lo, (int)hi, rv);
+      }
+    }
+    sm = s1;
+  }
+  flush();
 }
 
 // ---- Boruvka rounds over the maxima graph --------------------------------

@@ -467,10 +467,15 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         LTS_CUDA(cudaMemsetAsync(w.scal + SC_ECOUNT, 0, sizeof(int) * 2, s));
         LTS_CUDA(cudaMemsetAsync(w.bestP, 0, sizeof(unsigned long long) * n, s));
       }
-      if (c.g.ndim == 2)
-        k_edges<2><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
-      else
-        k_edges<3><<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
+      {
+        dim3 eg((c.g.nx + ET_TX - 1) / ET_TX, (c.g.ny + ET_TY - 1) / ET_TY,
+                c.g.ndim == 2 ? 1 : (c.g.nz + ET_ZC - 1) / ET_ZC);
+        dim3 eb3(ET_TX, ET_TY);
+        if (c.g.ndim == 2)
+          k_edges_tile<2><<<eg, eb3, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
+        else
+          k_edges_tile<3><<<eg, eb3, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
+      }
       g_launches++;
       if (mode == 0) {
         k_hash_compact<<<NB(1ll << hbits), 256, 0, s>>>(H, ea, eb, ew, w.scal + SC_TMP);
