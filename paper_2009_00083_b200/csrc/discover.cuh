@@ -289,6 +289,33 @@ __device__ __forceinline__ void edge_global(const EdgeHash &H, const uint8_t *__
   }
 }
 
+// shared edge table insert (one slot per unordered manifold pair, max
+// weight); a full probe window sends the edge straight to the global table
+__device__ __forceinline__ void et_insert(unsigned long long *hkey, int *hw, int *hcount,
+                                          const EdgeHash &H, const uint8_t *__restrict__ vcls,
+                                          unsigned long long *bestP, int *ea, int *eb, int *ew,
+                                          int *ecount, int a, int b, int w) {
+  const unsigned lo = (unsigned)min(a, b), hi = (unsigned)max(a, b);
+  const unsigned long long key = ((unsigned long long)lo << 32) | hi;
+  unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 53) & (ET_HT - 1);
+  bool done = false;
+  for (int probe = 0; probe < 32 && !done; probe++, h = (h + 1) & (ET_HT - 1)) {
+    unsigned long long kk = hkey[h];
+    if (kk == ~0ull) {
+      kk = atomicCAS(hkey + h, ~0ull, key);
+      if (kk == ~0ull) {
+        atomicAdd(hcount, 1);
+        kk = key;
+      }
+    }
+    if (kk == key) {
+      if (hw[h] < w) atomicMax(hw + h, w);
+      done = true;
+    }
+  }
+  if (!done) edge_global(H, vcls, bestP, ea, eb, ew, ecount, (int)lo, (int)hi, w);
+}
+
 template <int NDIM>
 __global__ void __launch_bounds__(ET_NT) k_edges_tile(Grid g, const int *__restrict__ rank, int rev,
                                                     const int *__restrict__ M,
@@ -382,9 +409,11 @@ __global__ void __launch_bounds__(ET_NT) k_edges_tile(Grid g, const int *__restr
     if (__syncthreads_or(tid == 0 && hcount > ET_FLUSH)) flush();
     const int *m0 = sM[NDIM == 2 ? 0 : s1], *mm = sM[NDIM == 2 ? 0 : sm], *mp = sM[NDIM == 2 ? 0 : s2];
     const int *r0 = sR[NDIM == 2 ? 0 : s1], *rm_ = sR[NDIM == 2 ? 0 : sm], *rp = sR[NDIM == 2 ? 0 : s2];
+    int a = -1, rv = -1;
+    int d0 = -1, d1 = -1, d2 = -1;  // distinct higher neighbour manifolds (first three)
     if (x < nx && y < ny) {
-      const int a = m0[c], rv = r0[c];
-      int d0 = -1, d1 = -1, d2 = -1;  // manifolds this vertex already sent
+      a = m0[c];
+      rv = r0[c];
 #pragma unroll
       for (int k = 0; k < K; k++) {
         const int dz = St::dz(k);
@@ -395,30 +424,24 @@ __global__ void __launch_bounds__(ET_NT) k_edges_tile(Grid g, const int *__restr
         if (b == a || b < 0) continue;
         if (rk[o] < rv) continue;                      // owned by the lower endpoint
         if (b == d0 || b == d1 || b == d2) continue;  // same weight rv: a duplicate
-        d2 = d1;
-        d1 = d0;
-        d0 = b;
-        // shared table: one slot per unordered manifold pair, max weight
-        const unsigned lo = (unsigned)min(a, b), hi = (unsigned)max(a, b);
-        const unsigned long long key = ((unsigned long long)lo << 32) | hi;
-        unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 53) & (ET_HT - 1);
-        bool done = false;
-        for (int probe = 0; probe < 32 && !done; probe++, h = (h + 1) & (ET_HT - 1)) {
-          unsigned long long kk = hkey[h];
-          if (kk == ~0ull) {
-            kk = atomicCAS(hkey + h, ~0ull, key);
-            if (kk == ~0ull) {
-              atomicAdd(&hcount, 1);
-              kk = key;
-            }
-          }
-          if (kk == key) {
-            if (hw[h] < rv) atomicMax(hw + h, rv);
-            done = true;
-          }
-        }
-        if (!done) edge_global(H, vcls, bestP, ea, eb, ew, ecount, (int)lo, (int)hi, rv);
+        if (d0 < 0) d0 = b;
+        else if (d1 < 0) d1 = b;
+        else if (d2 < 0) d2 = b;
+        else et_insert(hkey, hw, &hcount, H, vcls, bestP, ea, eb, ew, ecount, a, b, rv);  // rare
       }
+    }
+    // warp aggregation (32 consecutive x voxels usually border the same
+    // manifolds): one shared-table update per distinct pair and warp
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const int b = i == 0 ? d0 : (i == 1 ? d1 : d2);
+      const bool has = b >= 0;
+      if (!__any_sync(0xffffffffu, has)) break;
+      const unsigned lo = (unsigned)min(a, b), hi = (unsigned)max(a, b);
+      const unsigned long long key = has ? (((unsigned long long)lo << 32) | hi) : ~0ull;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int best = __reduce_max_sync(peers, rv);
+      if (has && rv == best) et_insert(hkey, hw, &hcount, H, vcls, bestP, ea, eb, ew, ecount, a, b, rv);
     }
     sm = s1;
   }
