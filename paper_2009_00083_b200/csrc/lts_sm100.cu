@@ -417,7 +417,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
   cudaStream_t s = c.s;
   lts_pass_report_t r{};
   r.kind = kind;
-  int R = 0, C = 0, S = 0;
+  int R = 0, C = 0, S = 0, nshared = 0;
   {
     Phase ph(c, LTS_PH_CLASSIFY);
     launch_classify(c.g, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
@@ -586,6 +586,32 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       else k_localize<3><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
       g_launches++;
     }
+    // Work that does not need the local orders runs while the large-region
+    // floods finish on the side stream: the integration prefix, the ranks of
+    // every unclaimed vertex (k_integrate_plain) and the numeric realization.
+    LTS_CUDA(cudaMemsetAsync(w.delta, 0, sizeof(int) * n, s));
+    k_delta_claimed<<<NB(C), 256, 0, s>>>(w.sval, C, rank, rev, ni, w.delta);
+    k_delta_saddles<<<NB(R), 256, 0, s>>>(w.rsad, w.rsize, R, w.delta);
+    k_count_shared<<<NB(R), 256, 0, s>>>(w.rsad, w.rsize, R, w.delta, w.scal + SC_NSHARED);
+    g_launches += 3;
+    LTS_TRY(scan_int(w.delta, w.D, n, w.bsum, w.scal + SC_TMP, true, s));
+    LTS_TRY(readback(c, SC_NSHARED, 1));
+    nshared = c.h_scal[SC_NSHARED];
+    r.shared_saddles = nshared;
+    if (nshared) {
+      k_iota<<<NB(R), 256, 0, s>>>(w.okey, R);  // reuse as values
+      g_launches++;
+      LTS_TRY(radix_sort((const uint32_t *)w.rsad, (const uint32_t *)w.okey, R, bits_for(n - 1), false,
+                         w.okey2, w.oval, nullptr, w.sb, s));
+      k_pos_of<<<NB(R), 256, 0, s>>>(w.oval, R, w.sib_rid, w.pos_of);
+      g_launches++;
+    }
+    k_integrate_plain<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.cbits, w.D, new_rank, new_inv);
+    g_launches++;
+    if (g) {
+      k_realize<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, g);
+      g_launches++;
+    }
     if (nbig > 0) LTS_TRY(big_stream_join(s));
     k_loc_stats<<<NB(R), 256, 0, s>>>(w.nit, w.st, w.rsize, R, w.scal + SC_STATS);
     g_launches += 1;
@@ -598,33 +624,9 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
   }
   {
     Phase ph(c, LTS_PH_INTEGRATE);
-    LTS_CUDA(cudaMemsetAsync(w.delta, 0, sizeof(int) * n, s));
-    k_delta_claimed<<<NB(C), 256, 0, s>>>(w.sval, C, rank, rev, ni, w.delta);
-    k_delta_saddles<<<NB(R), 256, 0, s>>>(w.rsad, w.rsize, R, w.delta);
-    k_count_shared<<<NB(R), 256, 0, s>>>(w.rsad, w.rsize, R, w.delta, w.scal + SC_NSHARED);
-    g_launches += 3;
-    LTS_TRY(scan_int(w.delta, w.D, n, w.bsum, w.scal + SC_TMP, true, s));
-    LTS_TRY(readback(c, SC_NSHARED, 1));
-    int nshared = c.h_scal[SC_NSHARED];
-    r.shared_saddles = nshared;
-    if (nshared) {
-      k_iota<<<NB(R), 256, 0, s>>>(w.okey, R);  // reuse as values
-      g_launches++;
-      LTS_TRY(radix_sort((const uint32_t *)w.rsad, (const uint32_t *)w.okey, R, bits_for(n - 1), false,
-                         w.okey2, w.oval, nullptr, w.sb, s));
-      k_pos_of<<<NB(R), 256, 0, s>>>(w.oval, R, w.sib_rid, w.pos_of);
-      g_launches++;
-    }
-    k_integrate_plain<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.cbits, w.D, new_rank, new_inv);
     k_integrate_regions<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.out, w.rsad, w.rsize, w.rtop,
                                               w.delta, w.D, w.sib_rid, w.pos_of, R, nshared, rev, ni,
                                               new_rank, new_inv);
-    g_launches += 2;
-    LTS_KCHECK();
-  }
-  if (g) {
-    Phase ph(c, LTS_PH_REALIZE);
-    k_realize<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, g);
     g_launches++;
     LTS_KCHECK();
   }
