@@ -3,21 +3,23 @@
 //
 // A priority flood's extraction order depends only on which vertices are in
 // the frontier F when each extraction happens.  Let f1 > f2 > ... be F sorted
-// by key and let new_i be the unseen neighbours exposed by extracting f1..fi.
+// by key and let new_i be the unseen neighbours exposed by extracting f_i.
 // Then f1..fj are the next j extractions, in that order, iff
 //     max key(new_1 u ... u new_i) < key(f_{i+1})   for every i < j.
-// Each step therefore takes the top-B keys of F, computes the exposure maxima
-// of all candidates in parallel (B x K neighbour probes), cuts the prefix at
-// the first preemption and commits it.  On the cfg3 regions a flood needs
-// ~1% as many steps as extractions.
+// Each step therefore takes the top-B keys of F (B = one per thread), every
+// thread loads its candidate's neighbour row and computes its exposure
+// maximum, one block-wide prefix-max scan finds the first preemption, and the
+// prefix is committed.  On the cfg3 regions a flood needs ~1% as many steps as
+// extractions, so the step's latency is the kernel's cost: a step is one
+// L2 round trip (the candidates' rows) plus shared-memory scans and four
+// barriers of BIG_T/32 warps.
 //
 // Keys are a permutation of a small integer range (the region's local order),
-// so F is a bit set over key space kept as a 32-ary bit tree in shared memory
-// (the leaf level spills to global memory for very large regions).  The top-B
-// keys come from a descending walk of the tree; key -> local index is an
-// inverse array rebuilt per flood; "seen" is a bit set over local indices.
-// Region adjacency is resolved once per region into rows of local indices so
-// every flood and check touches one row per vertex.
+// so F is a bit set over key space ("leaf" words, in shared memory unless the
+// region is very large); the top-B keys come from a descending chunked scan
+// of the leaf words, starting at the highest non-empty chunk.  "seen" is a bit
+// set over keys.  The neighbour rows of the flood are indexed by key and the
+// key -> local index map is rebuilt per flood by k_big_setup (grid-wide).
 // Semantics follow _localize_one (_kernels.py:443-575) exactly, including the
 // empty-ascending-flood case and the period-2 cycle jump (contract D5).
 #pragma once
@@ -26,17 +28,19 @@
 namespace lts {
 
 #ifndef LTS_BIG_T
-#define LTS_BIG_T 1024
+#define LTS_BIG_T 256
 #endif
-constexpr int BIG_T = LTS_BIG_T;
-#ifndef LTS_BIG_B
-#define LTS_BIG_B 256
+constexpr int BIG_T = LTS_BIG_T;              // threads per flood CTA
+constexpr int BIG_B = BIG_T;                  // candidates per step: one per thread
+constexpr int BIG_NW = BIG_T / 32;
+#ifndef LTS_BIG_WPT
+#define LTS_BIG_WPT 4
 #endif
-constexpr int BIG_B = LTS_BIG_B;              // max candidates per step
-constexpr int BIG_SMEM_WORDS = 10 * 1024;     // bit-set words in shared memory (rest of the SM is L1)
-constexpr int BIG_XMAX = 512;                 // climb continuation list (index fits 9 bits)
-static_assert(BIG_XMAX <= 512, "packed climb argmax");
-constexpr int BIG_HOPS = 16;                  // sequential hops per step
+constexpr int BIG_WPT = LTS_BIG_WPT;          // leaf words per thread in the candidate scan
+constexpr int BIG_CHUNK = BIG_T * BIG_WPT;    // leaf words per scan chunk
+constexpr int BIG_CHUNK_SHIFT = BIG_CHUNK == 512 ? 14 : BIG_CHUNK == 1024 ? 15 : BIG_CHUNK == 2048 ? 16 : 17;
+static_assert((32 * BIG_CHUNK) == (1 << BIG_CHUNK_SHIFT), "chunk = BIG_CHUNK leaf words");
+constexpr int BIG_SMEM_WORDS = 16 * 1024;     // bit-set words in shared memory (rest of the SM is L1)
 constexpr int BIG_THRESHOLD = 256;            // regions with k > this use this kernel
 
 struct BigArgs {
@@ -47,125 +51,29 @@ struct BigArgs {
   int *nrowkey;      // per key: K neighbour keys of the current flood (rows in key order)
   int qbase, nbig;   // regions order[qbase .. qbase+nbig)
   int *queue;
+  int *st;           // per big region: BST_W ints of flood state (below)
+  int *nactive;      // regions still flooding after the last decide
 };
 
+// per-region flood state, kept in global memory between the grid-wide
+// setup / check kernels and the one-CTA-per-region flood kernel
+enum { BST_T = 0, BST_ACTIVE, BST_FIN, BST_STATUS, BST_BAD, BST_DIFF, BST_W = 8 };
+
 // optional per-region instrumentation (lts_debug_big_stats): big-queue slot i
-// records [k, steps, candidates, committed, flood cycles, check cycles, init
-// cycles, n_iters]
+// records [k, steps, candidates, committed, flood cycles, -, -, n_iters,
+// gather, probe, cut, commit cycles]
 constexpr int DBG_MAX = 256, DBG_W = 24;
 __device__ long long d_dbg[DBG_MAX * DBG_W];
 __device__ int d_dbg_on;
 
-// Frontier F as a counted bit set over key space [0, k]: leaf bits plus, per
-// block of 32^(l+1) keys, the number of keys in F (levels 1..top).  The top
-// level has <= 32 blocks, so one warp reads it in one step.
-struct CTree {
-  uint32_t *leaf;
-  int nw0;          // leaf words
-  int *cnt[6];      // cnt[l][i], l = 1..top: keys in block i of level l
-  int nb[6];        // blocks per level (nb[0] = nw0)
-  int top;
-};
-
-__device__ __forceinline__ uint32_t mask_le(int b) { return b >= 31 ? 0xffffffffu : ((2u << b) - 1u); }
-
-__device__ __forceinline__ void ct_insert(const CTree &T, int key) {
-  atomicOr(T.leaf + (key >> 5), 1u << (key & 31));
-  for (int l = 1; l <= T.top; l++) atomicAdd(T.cnt[l] + (key >> (5 * (l + 1))), 1);
-}
-
-__device__ __forceinline__ void ct_remove(const CTree &T, int key) {
-  atomicAnd(T.leaf + (key >> 5), ~(1u << (key & 31)));
-  for (int l = 1; l <= T.top; l++) atomicSub(T.cnt[l] + (key >> (5 * (l + 1))), 1);
-}
-
-// warp-aggregated count updates: the upper levels have few blocks, so per-key
-// shared atomics would serialise on a handful of addresses
-__device__ __forceinline__ void ct_update_warp(const CTree &T, int key, bool valid, int delta) {
-  const unsigned act = __activemask();
-  const int lane = threadIdx.x & 31;
-  if (valid) {
-    if (delta > 0) atomicOr(T.leaf + (key >> 5), 1u << (key & 31));
-    else atomicAnd(T.leaf + (key >> 5), ~(1u << (key & 31)));
-  }
-  for (int l = 1; l <= T.top; l++) {
-    int idx = valid ? (key >> (5 * (l + 1))) : -1;
-    unsigned peers = __match_any_sync(act, idx);
-    if (valid && lane == __ffs(peers) - 1) atomicAdd(T.cnt[l] + idx, delta * __popc(peers));
-  }
-}
-
-// leaf-only frontier updates; the highest non-empty chunk (BIG_T leaf words)
-// is tracked with one warp-aggregated atomicMax per insertion batch
-__device__ __forceinline__ void leaf_remove(uint32_t *leaf, int key, bool valid) {
-  if (valid) atomicAnd(leaf + (key >> 5), ~(1u << (key & 31)));
-}
-
-__device__ __forceinline__ void leaf_insert(uint32_t *leaf, int *hi_chunk, int key, bool valid,
-                                            int chunk_shift) {
-  if (valid) atomicOr(leaf + (key >> 5), 1u << (key & 31));
-  const unsigned act = __activemask();
-  const int m = __reduce_max_sync(act, valid ? (key >> chunk_shift) : -1);
-  if (m >= 0 && (threadIdx.x & 31) == __ffs(act) - 1) atomicMax(hi_chunk, m);
-}
-
-// warp 0: the `need`-th largest key of F (need clamped to |F|).  Returns the
-// threshold key tau (-1 if F is empty) and the clamped need.
-__device__ __forceinline__ int ct_threshold(const CTree &T, int want, int &need_out) {
-  const int lane = threadIdx.x & 31;
-  int l = T.top, base = 0, nel = T.nb[T.top];
-  int need = want;
-  bool first = true;
-  for (;;) {
-    int e = base + nel - 1 - lane;
-    int c = 0;
-    if (lane < nel) c = l == 0 ? __popc(T.leaf[e]) : T.cnt[l][e];
-    int P = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, P, o);
-      if (lane >= o) P += y;
-    }
-    if (first) {
-      int total = __shfl_sync(0xffffffffu, P, 31);
-      need = min(need, total);
-      need_out = need;
-      if (need == 0) return -1;
-      first = false;
-    }
-    unsigned hit = __ballot_sync(0xffffffffu, P >= need);
-    int src = __ffs(hit) - 1;
-    int before = __shfl_sync(0xffffffffu, P - c, src);
-    int es = base + nel - 1 - src;
-    need -= before;
-    if (l == 0) {
-      uint32_t w = T.leaf[es];
-      // need-th highest set bit of w
-      int b = 31;
-      for (int r = 0;; b--) {
-        if ((w >> b) & 1u) {
-          if (++r == need) break;
-        }
-      }
-      return (es << 5) + b;
-    }
-    base = es << 5;
-    nel = min(32, T.nb[l - 1] - base);
-    l--;
-  }
-}
-
 struct BigSmem {
-  int cand_key[BIG_B];
-  int newmax[BIG_B];
-  int pair_key[BIG_B * kMaxK];
-  int wsum[BIG_T / 32 + 1];
-  int ncand, cut, nsrc, red, v0, qi, tau, carry, hi_chunk;
-  int xcnt, enew;           // climb continuation: exposures above the window
-  int xkey[BIG_XMAX];
-  CTree T;          // frontier descriptor (uniform; kept out of local memory)
+  int pref[BIG_T];
+  int wsum[BIG_NW];
+  int wmax[BIG_NW];
+  int cut, hi_chunk, nw, nw4;
+  uint32_t *leaf;   // frontier bit set over keys
   uint32_t *seen;   // bit set over keys
-  uint32_t bits[BIG_SMEM_WORDS];
+  __align__(16) uint32_t bits[BIG_SMEM_WORDS];
 };
 
 struct BigRegion {
@@ -177,10 +85,6 @@ struct BigRegion {
   int *inv;
 };
 
-__device__ __forceinline__ bool seen_test(const uint32_t *seen, int q) {
-  return (seen[q >> 5] >> (q & 31)) & 1u;
-}
-
 // desc floods map the sentinels +BIG -> k, -BIG -> 0; asc floods reverse
 __device__ __forceinline__ int flood_key(int c, bool asc, int k) {
   if (asc) return k - 1 - c;
@@ -189,9 +93,8 @@ __device__ __forceinline__ int flood_key(int c, bool asc, int k) {
   return c;
 }
 
-// block-wide exclusive scan (BIG_T threads) with one barrier: warp scans,
-// then every warp scans the warp totals itself.  The caller must barrier
-// before wsum is written again.
+// block-wide exclusive sum over threads in tid order, one barrier; the caller
+// barriers before wsum is written again
 __device__ __forceinline__ int big_scan_excl(int x, int *wsum, int &total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int inc = x;
@@ -202,350 +105,212 @@ __device__ __forceinline__ int big_scan_excl(int x, int *wsum, int &total) {
   }
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
-  const int v = lane < BIG_T / 32 ? wsum[lane] : 0;
-  int p = v;
+  int pre = 0, tot = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, p, o);
-    if (lane >= o) p += y;
+  for (int w = 0; w < BIG_NW; w++) {
+    const int v = wsum[w];
+    pre += w < warp ? v : 0;
+    tot += v;
   }
-  total = __shfl_sync(0xffffffffu, p, 31);
-  return __shfl_sync(0xffffffffu, p - v, warp) + inc - x;
+  total = tot;
+  return pre + inc - x;
 }
 
 template <int K>
-__device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, int *cout, int &Beff,
-                          long long *dbg) {
+__device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, int *cout, long long *dbg) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = G.k;
-  const CTree &T = S.T;
+  uint32_t *const leaf = S.leaf;
   uint32_t *const seen = S.seen;
-  const int seen_words = T.nw0;
-  for (int i = tid; i < T.nw0; i += BIG_T) T.leaf[i] = 0u;
-  for (int l = 1; l <= T.top; l++)
-    for (int i = tid; i < T.nb[l]; i += BIG_T) T.cnt[l][i] = 0;
-  for (int i = tid; i < seen_words; i += BIG_T) seen[i] = 0u;
+  const int nw = S.nw4;
+  for (int i = tid; i < nw; i += BIG_T) {
+    leaf[i] = 0u;
+    seen[i] = 0u;
+  }
   if (tid == 0) {
-    S.nsrc = 0;
     S.hi_chunk = -1;
+    S.cut = 0x7fffffff;
   }
   __syncthreads();
-  auto key_of = [&](int p) -> int { return flood_key(cin[p], asc, k); };
-  for (int p = tid; p < k; p += BIG_T) G.inv[key_of(p)] = p;
-  // neighbour keys of this flood, one row per KEY: the flood never needs a
-  // local index except to write its label
-  for (int i = tid; i < k * K; i += BIG_T) {
-    const int p = i / K, kk = i - p * K;
-    const int q = G.row[i];
-    G.krow[key_of(p) * K + kk] = q >= 0 ? key_of(q) : -1;
-  }
-  constexpr int CHUNK_SHIFT = BIG_T == 1024 ? 15 : BIG_T == 512 ? 14 : 13;  // BIG_T leaf words per chunk
-  static_assert((32 * BIG_T) == (1 << CHUNK_SHIFT), "chunk = BIG_T leaf words");
+  // sources: the saddle (desc) or every admissible boundary minimum (asc)
+  int mine = 0;
   if (!asc) {
-    if (warp == 0) {
-      const bool src = lane == 0;
-      const int key = key_of(0);
-      if (src) {
-        atomicOr(seen + (key >> 5), 1u << (key & 31));
-        S.nsrc = 1;
-      }
-      leaf_insert(T.leaf, &S.hi_chunk, key, src, CHUNK_SHIFT);
+    if (tid == 0) {
+      const int key = flood_key(cin[0], false, k);
+      seen[key >> 5] |= 1u << (key & 31);
+      leaf[key >> 5] |= 1u << (key & 31);
+      S.hi_chunk = key >> BIG_CHUNK_SHIFT;
+      mine = 1;
     }
   } else {
-    for (int p0 = 1; p0 < k; p0 += BIG_T) {
-      const int p = p0 + tid;
-      const bool src = p < k && (G.sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT);
-      const int key = src ? key_of(p) : 0;
-      if (src) {
+    int mch = -1;
+    for (int p = 1 + tid; p < k; p += BIG_T) {
+      if ((G.sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) {
+        const int key = flood_key(cin[p], true, k);
         atomicOr(seen + (key >> 5), 1u << (key & 31));
-        atomicAdd(&S.nsrc, 1);
+        atomicOr(leaf + (key >> 5), 1u << (key & 31));
+        mch = max(mch, key >> BIG_CHUNK_SHIFT);
+        mine = 1;
       }
-      leaf_insert(T.leaf, &S.hi_chunk, key, src, CHUNK_SHIFT);
     }
+    mch = __reduce_max_sync(0xffffffffu, mch);
+    if (lane == 0 && mch >= 0) atomicMax(&S.hi_chunk, mch);
   }
-  __syncthreads();
-  if (S.nsrc == 0) {  // empty ascending flood keeps the previous labels
+  if (__syncthreads_or(mine) == 0) {  // empty ascending flood keeps the previous labels
     for (int p = tid; p < k; p += BIG_T) cout[p] = cin[p];
     __syncthreads();
     return;
   }
   int e = 0;
-  // instrumentation accumulates in registers (a global += per tick would
-  // stall thread 0 on a load and perturb the barriers being measured)
-  long long tacc[DBG_W];
-#pragma unroll
-  for (int i = 0; i < DBG_W; i++) tacc[i] = 0;
-  long long tq = clock64(), tn;
-#define BIG_TICK(slot)                          \
-  if (dbg && tid == 0) {                        \
-    tn = clock64();                             \
-    dbg[slot] += tn - tq;                       \
-    tq = tn;                                    \
+  long long tq = 0, tn, tg = 0, tp = 0, tc = 0, tm = 0, nst = 0, ncand = 0;
+  if (dbg && tid == 0) tq = clock64();
+#define BIG_TICK(acc)      \
+  if (dbg && tid == 0) {   \
+    tn = clock64();        \
+    acc += tn - tq;        \
+    tq = tn;               \
   }
   for (;;) {
-    BIG_TICK(8)
-    if (tid == 0) S.xcnt = 0;
-    // (a) candidates = the top Beff keys of F.  The CTA scans leaf words in
-    // chunks of BIG_T words (one word per thread, thread 0 = highest word),
-    // skipping empty chunks with the level-2 counts; a block scan of the
-    // popcounts gives every key its descending rank.
-    int nc = 0;
+    // (a) candidates = the top B keys of F, descending, one per thread: a
+    // chunk of leaf words (thread 0 owns the highest BIG_WPT words) is
+    // popcounted and scanned once; then candidate slot i binary-searches the
+    // per-thread prefix for the owner of its key and selects the bit, so every
+    // thread does the same small amount of work however the keys cluster
+    int nc = 0, key = -1;
     {
       const int hi = S.hi_chunk;
       int top_found = -1;
-      for (int ch = hi; ch >= 0 && nc < Beff; ch--) {
-        const int w = ch * BIG_T + (BIG_T - 1 - tid);
-        uint32_t word = w < T.nw0 ? T.leaf[w] : 0u;
+      for (int ch = hi; ch >= 0 && nc < BIG_B; ch--) {
+        const int base = ch * BIG_CHUNK + (BIG_T - 1 - tid) * BIG_WPT;
+        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+        if (base < S.nw4) w = *reinterpret_cast<const uint4 *>(leaf + base);
+        const int cnt = __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
         int tot;
-        int r = nc + big_scan_excl(__popc(word), S.wsum, tot);
-        if (dbg && tid == 0) {
-          tn = clock64();
-          tacc[16] += 1;
-          tacc[17] += tn - tq;
-          tq = tn;
-        }
-        while (word && r < Beff) {
-          int b = 31 - __clz(word);
-          word &= ~(1u << b);
-          S.newmax[r] = -1;
-          S.cand_key[r++] = (w << 5) + b;
+        const int r = big_scan_excl(cnt, S.wsum, tot);
+        S.pref[tid] = r;
+        __syncthreads();
+        const int want = tid - nc;
+        if (want >= 0 && want < tot) {
+          int lo = 0, up = BIG_T - 1;  // owner: the last thread with pref <= want
+#pragma unroll
+          for (int it = 0; it < 16 && lo < up; it++) {
+            const int mid = (lo + up + 1) >> 1;
+            if (S.pref[mid] <= want) lo = mid;
+            else up = mid - 1;
+          }
+          int rem = want - S.pref[lo];
+          const int b0 = ch * BIG_CHUNK + (BIG_T - 1 - lo) * BIG_WPT;
+          const uint4 ow = *reinterpret_cast<const uint4 *>(leaf + b0);
+          const uint32_t ws[4] = {ow.w, ow.z, ow.y, ow.x};  // highest word first
+          int u = 3;
+#pragma unroll
+          for (int h = 0; h < 4; h++) {
+            const int c = __popc(ws[h]);
+            if (rem < c) {
+              u = 3 - h;
+              const uint32_t x = ws[h];
+              const int need = rem + 1;  // need-th highest set bit of x
+              int bpos = 0;
+#pragma unroll
+              for (int sft = 16; sft >= 1; sft >>= 1)
+                if (__popc(x >> (bpos + sft)) >= need) bpos += sft;
+              key = ((b0 + u) << 5) + bpos;
+              break;
+            }
+            rem -= c;
+          }
         }
         if (tot > 0 && top_found < 0) top_found = ch;
-        nc = min(Beff, nc + tot);
-        __syncthreads();
-        if (dbg && tid == 0) {
-          tn = clock64();
-          tacc[18] += tn - tq;
-          tq = tn;
-        }
+        nc = min(BIG_B, nc + tot);
       }
-      // chunks above the first non-empty one are empty: start lower next time
-      if (tid == 0) S.hi_chunk = top_found;
+      if (tid == 0) S.hi_chunk = top_found;  // chunks above it are empty
     }
-    BIG_TICK(9)
+    BIG_TICK(tg)
     if (nc == 0) break;
-    if (tid == 0) S.cut = nc;
-    // the label slot of candidate tid, in flight until the commit (BIG_B <= BIG_T)
-    const int cand_p = tid < nc ? G.inv[S.cand_key[tid]] : 0;
-    BIG_TICK(10)
-    // (b) exposure maxima of every candidate: all row loads issued first
-    {
-      constexpr int PPT = (BIG_B * K + BIG_T - 1) / BIG_T;
-      int nk[PPT];
+    // (b) probes: thread i owns candidate i; its row of neighbour keys and
+    // its local index come from L2 in one round trip
+    const bool isc = tid < nc;
+    int q[K];
+    int cand_p = 0;
+    if (isc) {
+      cand_p = G.inv[key];
+      const int2 *row = reinterpret_cast<const int2 *>(G.krow + (size_t)key * K);
 #pragma unroll
-      for (int t = 0; t < PPT; t++) {
-        const int i = tid + t * BIG_T;
-        nk[t] = -1;
-        if (i < nc * K) {
-          const int c = i / K;
-          nk[t] = G.krow[S.cand_key[c] * K + (i - c * K)];
-        }
+      for (int h = 0; h < K / 2; h++) {
+        const int2 v = row[h];
+        q[2 * h] = v.x;
+        q[2 * h + 1] = v.y;
       }
+    } else {
 #pragma unroll
-      for (int t = 0; t < PPT; t++) {
-        const int i = tid + t * BIG_T;
-        if (i < nc * K) {
-          int q = nk[t];
-          if (q >= 0 && !seen_test(seen, q)) atomicMax(&S.newmax[i / K], q);
-          else q = -1;
-          S.pair_key[i] = q;
-        }
-      }
+      for (int kk = 0; kk < K; kk++) q[kk] = -1;
     }
-    __syncthreads();
-    BIG_TICK(11)
-    // (c) prefix max and first preemption: warp 0, 8 candidates per lane
-    if (warp == 0) {
-      constexpr int PER = BIG_B / 32;
-      int loc[PER];
-      int m = -1;
+    int nm = -1;
 #pragma unroll
-      for (int t = 0; t < PER; t++) {
-        int i = lane * PER + t;
-        int v = i < nc ? S.newmax[i] : -1;
-        m = max(m, v);
-        loc[t] = m;
-      }
-      int P = m;  // inclusive scan of lane maxima
+    for (int kk = 0; kk < K; kk++) {
+      const int x = q[kk];
+      if (x >= 0 && !((seen[x >> 5] >> (x & 31)) & 1u)) nm = max(nm, x);
+      else q[kk] = -1;
+    }
+    BIG_TICK(tp)
+    // (c) first preemption: exclusive prefix max of the exposures in
+    // candidate order against the candidate's own key
+    {
+      int inc = nm;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, P, o);
-        if (lane >= o) P = max(P, y);
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = max(inc, y);
       }
-      int carry = __shfl_up_sync(0xffffffffu, P, 1);
-      if (lane == 0) carry = -1;
-      int first = 0x7fffffff;
-#pragma unroll
-      for (int t = 0; t < PER; t++) {
-        int i = lane * PER + t;
-        if (i + 1 < nc && max(carry, loc[t]) > S.cand_key[i + 1] && first == 0x7fffffff) first = i + 1;
-      }
-      first = __reduce_min_sync(0xffffffffu, first);
-      if (lane == 0 && first != 0x7fffffff) S.cut = first;
-    }
-    __syncthreads();
-    BIG_TICK(12)
-    const int j = S.cut;
-    // (d) commit the prefix: labels, leave F; its exposures join F
-    {
-      const bool v = tid < j;
-      if (v) cout[cand_p] = asc ? (e + tid) : (k - 1 - (e + tid));
-      leaf_remove(T.leaf, v ? S.cand_key[tid] : 0, v);
-    }
-    BIG_TICK(13)
-    const int kappa = S.cand_key[nc - 1];  // every key of F above kappa is known
-    for (int i0 = 0; i0 < j * K; i0 += BIG_T) {
-      int i = i0 + tid;
-      int q = i < j * K ? S.pair_key[i] : -1;
-      bool ins = false;
-      if (q >= 0) {
-        uint32_t bit = 1u << (q & 31);
-        ins = !(atomicOr(seen + (q >> 5), bit) & bit);
-      }
-      leaf_insert(T.leaf, &S.hi_chunk, ins ? q : 0, ins, CHUNK_SHIFT);
-      if (ins && q > kappa) {
-        int x = atomicAdd(&S.xcnt, 1);
-        if (x < BIG_XMAX) S.xkey[x] = q;
-      }
-    }
-    e += j;
-    if (dbg && tid == 0) {
-      tacc[1] += 1;
-      tacc[2] += nc;
-      tacc[3] += j;
-    }
-    if (j == nc && nc == Beff && Beff < BIG_B) Beff *= 2;
-    else if (j * 4 < Beff && Beff > 8) Beff >>= 1;
-    __syncthreads();
-    BIG_TICK(14)
-    // (e) climb continuation (warp 0): while the largest known exposure beats
-    // the next candidate, it IS the next extraction; follow it with one row
-    // load per hop instead of a full CTA step.  Exposures above kappa join
-    // the known list; everything else stays in the bit set.
-    const int xc = S.xcnt;
-    if (j <= 4 && xc > 0 && xc <= BIG_XMAX) {  // block-uniform: climbs only
-      if (dbg && tid == 0) tacc[19] += 1;
-      if (warp == 0) {
-        const int bound = j < nc ? S.cand_key[j] : kappa;
-        int m = xc, ee = e;
-        for (int hop = 0; hop < BIG_HOPS && m > 0; hop++) {
-          // argmax of the known list (keys are distinct): one packed
-          // (key, index) reduction when keys fit in 23 bits
-          int bk = -1, bi = 0x7fffffff;
-          if (k < (1 << 22)) {
-            unsigned pk = 0u;
-            for (int i = lane; i < m; i += 32) pk = max(pk, ((unsigned)(S.xkey[i] + 1) << 9) | (unsigned)i);
-            pk = __reduce_max_sync(0xffffffffu, pk);
-            bk = (int)(pk >> 9) - 1;
-            bi = (int)(pk & 511u);
-          } else {
-            for (int i = lane; i < m; i += 32) bk = max(bk, S.xkey[i]);
-            bk = __reduce_max_sync(0xffffffffu, bk);
-            for (int i = lane; i < m; i += 32)
-              if (S.xkey[i] == bk) bi = i;
-            bi = __reduce_min_sync(0xffffffffu, bi);
-          }
-          if (bk <= bound) break;
-          const int key2 = lane < K ? G.krow[bk * K + lane] : -1;
-          __syncwarp();
-          if (lane == 0) {
-            cout[G.inv[bk]] = asc ? ee : (k - 1 - ee);
-            S.xkey[bi] = S.xkey[m - 1];
-          }
-          leaf_remove(T.leaf, bk, lane == 0);
-          ee++;
-          m--;
-          __syncwarp();
-          bool ins = false;
-          if (key2 >= 0) {
-            uint32_t bit = 1u << (key2 & 31);
-            ins = !(atomicOr(seen + (key2 >> 5), bit) & bit);
-          }
-          leaf_insert(T.leaf, &S.hi_chunk, ins ? key2 : 0, ins, CHUNK_SHIFT);
-          const bool add = ins && key2 > kappa;
-          const unsigned am = __ballot_sync(0xffffffffu, add);
-          if (m + __popc(am) > BIG_XMAX) break;  // list full: leave the rest to the CTA
-          if (add) S.xkey[m + __popc(am & lanemask_lt())] = key2;
-          m += __popc(am);
-          __syncwarp();
-        }
-        if (lane == 0) S.enew = ee;
-      }
+      if (lane == 31) S.wmax[warp] = inc;
       __syncthreads();
-      if (dbg && tid == 0) tacc[15] += S.enew - e;
-      e = S.enew;
+      int pre = -1;
+#pragma unroll
+      for (int w = 0; w < BIG_NW; w++)
+        if (w < warp) pre = max(pre, S.wmax[w]);
+      int ex = __shfl_up_sync(0xffffffffu, inc, 1);
+      ex = lane == 0 ? pre : max(pre, ex);
+      const unsigned bal = __ballot_sync(0xffffffffu, isc && tid > 0 && ex > key);
+      if (lane == 0 && bal) atomicMin(&S.cut, warp * 32 + __ffs(bal) - 1);
+      __syncthreads();
     }
+    const int j = min(S.cut, nc);
+    BIG_TICK(tc)
+    // (d) commit the prefix: labels, leave F; its exposures join F (setting a
+    // bit twice is harmless, so the updates need no return value)
+    int mch = -1;
+    if (tid < j) {
+      cout[cand_p] = asc ? (e + tid) : (k - 1 - (e + tid));
+      atomicAnd(leaf + (key >> 5), ~(1u << (key & 31)));
+#pragma unroll
+      for (int kk = 0; kk < K; kk++) {
+        const int x = q[kk];
+        if (x >= 0) {
+          atomicOr(seen + (x >> 5), 1u << (x & 31));
+          atomicOr(leaf + (x >> 5), 1u << (x & 31));
+          mch = max(mch, x >> BIG_CHUNK_SHIFT);
+        }
+      }
+    }
+    mch = __reduce_max_sync(0xffffffffu, mch);
+    if (lane == 0 && mch >= 0) atomicMax(&S.hi_chunk, mch);
+    e += j;
+    nst++;
+    ncand += nc;
+    __syncthreads();
+    if (tid == 0) S.cut = 0x7fffffff;
+    BIG_TICK(tm)
   }
 #undef BIG_TICK
   if (dbg && tid == 0) {
-#pragma unroll
-    for (int i = 1; i < DBG_W; i++)
-      if (i < 4 || i > 7) dbg[i] += tacc[i];
+    dbg[1] += nst;
+    dbg[2] += ncand;
+    dbg[3] += e;
+    dbg[8] += tg;
+    dbg[9] += tp;
+    dbg[10] += tc;
+    dbg[11] += tm;
   }
-}
-
-// after a descending flood: SF_MIN marks, true if an unauthorized minimum
-template <int K>
-__device__ bool big_check_minima(BigSmem &S, BigRegion &G, const int *cur) {
-  if (threadIdx.x == 0) S.red = 0;
-  __syncthreads();
-  bool bad = false;
-  for (int p = 1 + threadIdx.x; p < G.k; p += BIG_T) {
-    const int *row = G.row + p * K;
-    int c = cur[p];
-    bool mn = true;
-#pragma unroll
-    for (int kk = 0; kk < K; kk++) {
-      int q = row[kk];
-      if (q >= 0 && cur[q] < c) mn = false;
-    }
-    uint8_t f = G.sfl[p];
-    f = mn ? (f | SF_MIN) : (f & (uint8_t)~SF_MIN);
-    G.sfl[p] = f;
-    if (mn && !(f & SF_OUT)) bad = true;
-  }
-  if (bad) atomicOr(&S.red, 1);
-  __syncthreads();
-  bool r = S.red != 0;
-  __syncthreads();
-  return r;
-}
-
-// after an ascending flood: true if a vertex other than the saddle is a max
-template <int K>
-__device__ bool big_check_maxima(BigSmem &S, BigRegion &G, const int *cur) {
-  if (threadIdx.x == 0) S.red = 0;
-  __syncthreads();
-  bool bad = false;
-  for (int p = 1 + threadIdx.x; p < G.k; p += BIG_T) {
-    const int *row = G.row + p * K;
-    int c = cur[p];
-    bool mx = true;
-#pragma unroll
-    for (int kk = 0; kk < K; kk++) {
-      int q = row[kk];
-      if (q >= 0 && cur[q] > c) mx = false;
-    }
-    if (mx) bad = true;
-  }
-  if (bad) atomicOr(&S.red, 1);
-  __syncthreads();
-  bool r = S.red != 0;
-  __syncthreads();
-  return r;
-}
-
-__device__ bool big_states_equal(BigSmem &S, const int *a, const int *b, int k) {
-  if (threadIdx.x == 0) S.red = 0;
-  __syncthreads();
-  bool diff = false;
-  for (int p = threadIdx.x; p < k; p += BIG_T)
-    if (a[p] != b[p]) diff = true;
-  if (diff) atomicOr(&S.red, 1);
-  __syncthreads();
-  bool r = S.red == 0;
-  __syncthreads();
-  return r;
 }
 
 // Region adjacency rows, has_outside flags, identity initial order and v0 for
@@ -581,139 +346,231 @@ __global__ void __launch_bounds__(256) k_big_rows(LocArgs A, BigArgs Bg) {
   if ((threadIdx.x & 31) == 0 && mine != 0x7fffffff) atomicMin(Bg.v0 + qi, mine);
 }
 
+// The big-region floods run as an iteration of four launches over all large
+// regions at once, so the per-flood work that is not the priority flood
+// itself (relabelling the neighbour rows, the constraint checks) is spread
+// over the whole GPU instead of one SM per region:
+//   k_big_setup   (grid-wide)  key -> local index and neighbour keys of flood t
+//   k_big_flood   (CTA/region) the exact batched priority flood t -> t+1
+//   k_big_check   (grid-wide)  unauthorized extrema of state t+1, and whether
+//                              state t+1 equals state t-1 (period-2 cycle)
+//   k_big_decide  (per region) _localize_one's stopping rules
+// The host repeats the iteration while a region is still flooding.
+
+__device__ __forceinline__ int *big_buf(const LocArgs &A, int i) {
+  const int m = i % 3;
+  return m == 0 ? A.buf0 : (m == 1 ? A.buf1 : A.buf2);
+}
+
+struct BigRef {
+  int rid, lo, k;
+};
+
+__device__ __forceinline__ BigRef big_ref(const LocArgs &A, const BigArgs &Bg, int qi) {
+  BigRef r;
+  r.rid = A.order[Bg.qbase + qi];
+  r.lo = A.rptr[r.rid];
+  r.k = A.rptr[r.rid + 1] - r.lo;
+  return r;
+}
+
+// per region: v0 from k_big_rows; no admissible minimum -> status 1
+__global__ void k_big_init(LocArgs A, BigArgs Bg) {
+  GRID_STRIDE(qi, Bg.nbig) {
+    const BigRef R = big_ref(A, Bg, (int)qi);
+    const int v0 = Bg.v0[qi];
+    int *st = Bg.st + qi * BST_W;
+    st[BST_T] = 0;
+    st[BST_BAD] = 0;
+    st[BST_DIFF] = 0;
+    if (v0 == 0x7fffffff) {
+      st[BST_ACTIVE] = 0;
+      st[BST_FIN] = -1;
+      st[BST_STATUS] = 1;
+    } else {
+      st[BST_ACTIVE] = 1;
+      st[BST_FIN] = 0;
+      st[BST_STATUS] = 0;
+      A.buf0[R.lo] = 0x7fffffff;
+      A.buf0[R.lo + v0] = (int)0x80000000;
+    }
+  }
+}
+
+// grid (chunks, regions): inverse and neighbour keys of the next flood.  One
+// row per thread, the K label gathers of a row independent of each other.
 template <int NDIM>
-__global__ void __launch_bounds__(BIG_T) k_localize_big(LocArgs A, BigArgs Bg) {
+__global__ void __launch_bounds__(256) k_big_setup(LocArgs A, BigArgs Bg) {
+  constexpr int K = NDIM == 2 ? 6 : 14;
+  static_assert(K % 2 == 0, "rows are read and written as int2");
+  const int qi = blockIdx.y;
+  const int *st = Bg.st + qi * BST_W;
+  if (!st[BST_ACTIVE]) return;
+  const int t = st[BST_T];
+  const bool asc = t & 1;
+  const BigRef R = big_ref(A, Bg, qi);
+  const int k = R.k;
+  const int *cin = big_buf(A, t) + R.lo;
+  int *inv = Bg.inv + R.lo + R.rid;
+  int *krow = Bg.nrowkey + ((size_t)R.lo + R.rid) * K;
+  const int *rows = Bg.nrow + (size_t)R.lo * K;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < k; p += gridDim.x * blockDim.x) {
+    const int kp = flood_key(cin[p], asc, k);
+    inv[kp] = p;
+    const int2 *row = reinterpret_cast<const int2 *>(rows + (size_t)p * K);
+    int q[K], c[K];
+#pragma unroll
+    for (int h = 0; h < K / 2; h++) {
+      const int2 v = row[h];
+      q[2 * h] = v.x;
+      q[2 * h + 1] = v.y;
+    }
+#pragma unroll
+    for (int kk = 0; kk < K; kk++) c[kk] = q[kk] >= 0 ? cin[q[kk]] : 0;
+    int2 *dst = reinterpret_cast<int2 *>(krow + (size_t)kp * K);
+#pragma unroll
+    for (int h = 0; h < K / 2; h++)
+      dst[h] = make_int2(q[2 * h] >= 0 ? flood_key(c[2 * h], asc, k) : -1,
+                         q[2 * h + 1] >= 0 ? flood_key(c[2 * h + 1], asc, k) : -1);
+  }
+}
+
+// one CTA per region (grid = regions, largest first): flood t -> t+1
+template <int NDIM>
+__global__ void __launch_bounds__(BIG_T) k_big_flood(LocArgs A, BigArgs Bg) {
   constexpr int K = NDIM == 2 ? 6 : 14;
   extern __shared__ __align__(16) unsigned char smraw[];
   BigSmem &S = *reinterpret_cast<BigSmem *>(smraw);
   const int tid = threadIdx.x;
-  const int n = (int)A.g.n;
-  for (;;) {
-    if (tid == 0) S.qi = atomicAdd(Bg.queue, 1);
-    __syncthreads();
-    const int qi = S.qi;
-    __syncthreads();
-    if (qi >= Bg.nbig) break;
-    BigRegion G;
-    G.rid = A.order[Bg.qbase + qi];
-    G.lo = A.rptr[G.rid];
-    G.k = A.rptr[G.rid + 1] - G.lo;
-    G.verts = A.verts + G.lo;
-    G.sfl = A.sfl + G.lo;
-    G.inv = Bg.inv + G.lo + G.rid;
-    G.row = Bg.nrow + (size_t)G.lo * K;
-    G.krow = Bg.nrowkey + ((size_t)G.lo + G.rid) * K;
-    G.s = G.verts[0];
-    const int k = G.k, rid = G.rid, lo = G.lo;
-    int *const b0 = A.buf0 + lo, *const b1 = A.buf1 + lo, *const b2 = A.buf2 + lo;
-#define BUF(i) ((i) % 3 == 0 ? b0 : ((i) % 3 == 1 ? b1 : b2))
-    // shared-memory layout: counts, leaf bits (if they fit), seen bits
-    if (tid == 0) {
-      CTree &T = S.T;
-      T.nw0 = (k + 1 + 31) >> 5;
-      T.nb[0] = T.nw0;
-      int l = 0;
-      while (T.nb[l] > 32) {
-        T.nb[l + 1] = (T.nb[l] + 31) >> 5;
-        l++;
-      }
-      T.top = l;
-      uint32_t *sp = S.bits;
-      int used = 0;
-      const int seen_words = T.nw0;
-      uint32_t *gp = Bg.gbits + 3 * (((size_t)lo + rid + 31) >> 5) + 8 * (size_t)rid;
-      int ncnt = 0;
-      for (int i = 1; i <= T.top; i++) ncnt += T.nb[i];
-      const bool cnt_smem = ncnt <= BIG_SMEM_WORDS;  // else every level in global
-      for (int i = 1; i <= T.top; i++) {
-        if (cnt_smem) {
-          T.cnt[i] = (int *)sp;
-          sp += T.nb[i];
-          used += T.nb[i];
-        } else {
-          T.cnt[i] = (int *)gp;
-          gp += T.nb[i];
-        }
-      }
-      if (used + T.nw0 <= BIG_SMEM_WORDS) {
-        T.leaf = sp;
-        sp += T.nw0;
-        used += T.nw0;
-      } else {
-        T.leaf = gp;
-        gp += T.nw0;
-      }
-      S.seen = (used + seen_words <= BIG_SMEM_WORDS) ? sp : gp;
+  const int qi = blockIdx.x;
+  int *st = Bg.st + qi * BST_W;
+  if (!st[BST_ACTIVE]) return;
+  const int t = st[BST_T];
+  BigRegion G;
+  G.rid = A.order[Bg.qbase + qi];
+  G.lo = A.rptr[G.rid];
+  G.k = A.rptr[G.rid + 1] - G.lo;
+  G.verts = A.verts + G.lo;
+  G.sfl = A.sfl + G.lo;
+  G.inv = Bg.inv + G.lo + G.rid;
+  G.row = Bg.nrow + (size_t)G.lo * K;
+  G.krow = Bg.nrowkey + ((size_t)G.lo + G.rid) * K;
+  G.s = G.verts[0];
+  const int k = G.k, rid = G.rid, lo = G.lo;
+  // bit sets in shared memory when they fit (the leaf words first: the
+  // candidate scan reads them every step), else in the region's spill space
+  if (tid == 0) {
+    const int nw = (k + 1 + 31) >> 5;
+    uint32_t *gp = Bg.gbits + ((3 * (((size_t)lo + rid + 31) >> 5) + 8 * (size_t)rid + 3) & ~(size_t)3);
+    const int nw4 = (nw + 3) & ~3;  // leaf read as uint4; padding stays zero
+    S.nw = nw;
+    S.nw4 = nw4;
+    S.leaf = nw4 <= BIG_SMEM_WORDS ? S.bits : gp;
+    S.seen = 2 * nw4 <= BIG_SMEM_WORDS ? S.bits + nw4 : gp + nw4;
+  }
+  __syncthreads();
+  const int qa = Bg.qbase + qi;  // absolute big-queue position
+  long long *dbg = (d_dbg_on && qa < DBG_MAX) ? d_dbg + qa * DBG_W : nullptr;
+  if (dbg && tid == 0) dbg[0] = k;
+  const long long c0 = clock64();
+  big_flood<K>(S, G, t & 1, big_buf(A, t) + lo, big_buf(A, t + 1) + lo, dbg);
+  if (dbg && tid == 0) dbg[4] += clock64() - c0;
+}
+
+// grid (chunks, regions): constraint check of state t+1 (desc flood: local
+// minima get SF_MIN, unauthorized if not SF_OUT; asc flood: any local maximum
+// besides the saddle) and, from t+1 >= 3 on, state t+1 != state t-1
+template <int NDIM>
+__global__ void __launch_bounds__(256) k_big_check(LocArgs A, BigArgs Bg) {
+  constexpr int K = NDIM == 2 ? 6 : 14;
+  const int qi = blockIdx.y;
+  int *st = Bg.st + qi * BST_W;
+  if (!st[BST_ACTIVE]) return;
+  const int t1 = st[BST_T] + 1;
+  const bool desc = (t1 & 1) == 1;  // flood t1-1 was descending
+  const BigRef R = big_ref(A, Bg, qi);
+  const int *cur = big_buf(A, t1) + R.lo;
+  const int *old = big_buf(A, t1 + 1) + R.lo;  // state t1-2
+  const int *rows = Bg.nrow + (size_t)R.lo * K;
+  uint8_t *sfl = A.sfl + R.lo;
+  bool bad = false, diff = false;
+  for (int p = 1 + blockIdx.x * blockDim.x + threadIdx.x; p < R.k; p += gridDim.x * blockDim.x) {
+    const int2 *row = reinterpret_cast<const int2 *>(rows + (size_t)p * K);
+    const int c = cur[p];
+    int q[K];
+#pragma unroll
+    for (int h = 0; h < K / 2; h++) {
+      const int2 v = row[h];
+      q[2 * h] = v.x;
+      q[2 * h + 1] = v.y;
     }
-    __syncthreads();
-    const int qa = Bg.qbase + qi;  // absolute big-queue position
-    long long *dbg = (d_dbg_on && qa < DBG_MAX) ? d_dbg + qa * DBG_W : nullptr;
-    long long c0 = clock64(), c1;
-    // rows, has_outside and v0 were produced by k_big_rows (grid-wide)
-    if (tid == 0) S.v0 = Bg.v0[qa];
-    __syncthreads();
-    const int v0 = S.v0;
-    if (v0 == 0x7fffffff) {
-      for (int p = tid; p < k; p += BIG_T) A.out[lo + p] = p;
-      if (tid == 0) {
-        A.status[rid] = 1;
-        A.n_iters[rid] = 0;
-      }
-      __syncthreads();
-      continue;
+    bool ext = true;
+#pragma unroll
+    for (int kk = 0; kk < K; kk++)
+      if (q[kk] >= 0 && (desc ? cur[q[kk]] < c : cur[q[kk]] > c)) ext = false;
+    if (desc) {
+      uint8_t f = sfl[p];
+      f = ext ? (f | SF_MIN) : (f & (uint8_t)~SF_MIN);
+      sfl[p] = f;
+      if (ext && !(f & SF_OUT)) bad = true;
+    } else if (ext) {
+      bad = true;
     }
-    if (tid == 0) {
-      b0[0] = 0x7fffffff;
-      b0[v0] = (int)0x80000000;
-      if (dbg) dbg[0] = k;
+    if (t1 >= 3 && c != old[p]) diff = true;
+  }
+  // p = 0 (the saddle) takes part only in the cycle comparison
+  if (t1 >= 3 && blockIdx.x == 0 && threadIdx.x == 0 && cur[0] != old[0]) diff = true;
+  bad = __any_sync(0xffffffffu, bad);
+  diff = __any_sync(0xffffffffu, diff);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicOr(st + BST_BAD, 1);
+    if (diff) atomicOr(st + BST_DIFF, 1);
+  }
+}
+
+// per region: the stopping rules of _localize_one (_kernels.py:491-571) with
+// the period-2 cycle jump (contract D5); counts the regions still flooding
+__global__ void k_big_decide(LocArgs A, BigArgs Bg) {
+  GRID_STRIDE(qi, Bg.nbig) {
+    int *st = Bg.st + qi * BST_W;
+    if (!st[BST_ACTIVE]) continue;
+    int t = st[BST_T] + 1;
+    const bool bad = st[BST_BAD] != 0, diff = st[BST_DIFF] != 0;
+    st[BST_BAD] = 0;
+    st[BST_DIFF] = 0;
+    bool done = true;
+    if (!bad) {
+      st[BST_FIN] = t;
+    } else if (t >= A.max_iter) {
+      st[BST_STATUS] = 2;
+      st[BST_FIN] = t;
+    } else if (t >= 3 && !diff) {
+      st[BST_STATUS] = 2;
+      st[BST_FIN] = ((A.max_iter - t) % 2 == 0) ? t : t - 1;
+      t = A.max_iter;
+    } else {
+      done = false;
     }
-    __syncthreads();
-    c1 = clock64();
-    if (dbg && tid == 0) dbg[6] += c1 - c0;
-    int t = 0, status = 0, fin = 0, Beff = 32;
-    for (;;) {
-      c1 = clock64();
-      big_flood<K>(S, G, false, BUF(t), BUF(t + 1), Beff, dbg);
-      c0 = clock64();
-      if (dbg && tid == 0) dbg[4] += c0 - c1;
-      t++;
-      bool bad = big_check_minima<K>(S, G, BUF(t));
-      c1 = clock64();
-      if (dbg && tid == 0) dbg[5] += c1 - c0;
-      if (!bad) { fin = t; break; }
-      if (t >= A.max_iter) { status = 2; fin = t; break; }
-      if (t >= 3 && big_states_equal(S, BUF(t), BUF(t + 1), k)) {
-        status = 2;
-        fin = ((A.max_iter - t) % 2 == 0) ? t : t - 1;
-        t = A.max_iter;
-        break;
-      }
-      c1 = clock64();
-      big_flood<K>(S, G, true, BUF(t), BUF(t + 1), Beff, dbg);
-      c0 = clock64();
-      if (dbg && tid == 0) dbg[4] += c0 - c1;
-      t++;
-      bad = big_check_maxima<K>(S, G, BUF(t));
-      c1 = clock64();
-      if (dbg && tid == 0) dbg[5] += c1 - c0;
-      if (!bad) { fin = t; break; }
-      if (t >= A.max_iter) { status = 2; fin = t; break; }
-      if (t >= 3 && big_states_equal(S, BUF(t), BUF(t + 1), k)) {
-        status = 2;
-        fin = ((A.max_iter - t) % 2 == 0) ? t : t - 1;
-        t = A.max_iter;
-        break;
-      }
-    }
-    const int *fb = BUF(fin);
-#undef BUF
-    for (int p = tid; p < k; p += BIG_T) A.out[lo + p] = fb[p];
-    if (tid == 0) {
-      A.status[rid] = status;
-      A.n_iters[rid] = t;
-      if (dbg) dbg[7] = t;
-    }
-    __syncthreads();
+    st[BST_T] = t;
+    if (done) st[BST_ACTIVE] = 0;
+    else atomicAdd(Bg.nactive, 1);
+  }
+}
+
+// grid (chunks, regions): final local order, status and flood count
+__global__ void __launch_bounds__(256) k_big_final(LocArgs A, BigArgs Bg) {
+  const int qi = blockIdx.y;
+  const int *st = Bg.st + qi * BST_W;
+  const BigRef R = big_ref(A, Bg, qi);
+  const int fin = st[BST_FIN];
+  const int *fb = fin >= 0 ? big_buf(A, fin) + R.lo : nullptr;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < R.k; p += gridDim.x * blockDim.x)
+    A.out[R.lo + p] = fb ? fb[p] : p;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.status[R.rid] = st[BST_STATUS];
+    A.n_iters[R.rid] = st[BST_T];
+    const int qa = Bg.qbase + qi;
+    if (d_dbg_on && qa < DBG_MAX) d_dbg[qa * DBG_W + 7] = st[BST_T];
   }
 }
 

@@ -176,7 +176,7 @@ struct WS {
   int *verts, *buf0, *buf1, *buf2, *out;
   unsigned long long *gheap;
   uint8_t *sfl;
-  int *binv, *nrow, *nrowkey, *bigv0;
+  int *binv, *nrow, *nrowkey, *bigv0, *bst;
   uint32_t *cbits;
   uint32_t *gbits;
   rs::Bufs sb;
@@ -204,6 +204,7 @@ enum {
   SC_NBIG = 29,
   SC_BIGQ = 30,
   SC_LARGEST = 31,
+  SC_BIGACT = 32,
   SC_N = 64
 };
 
@@ -240,6 +241,7 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->sfl = (uint8_t *)take((size_t)s2);
   w->binv = i32(3 * n + 8);
   w->bigv0 = i32(n1);
+  w->bst = i32(BST_W * (n1 / BIG_THRESHOLD + 2));  // regions with k > BIG_THRESHOLD
   w->cbits = u32(n / 32 + 64);
   w->gbits = u32(6 * n + 64);
   w->nrow = i32((ndim == 2 ? 6 : 14) * s2);
@@ -371,35 +373,60 @@ __global__ void k_count_big(const int *rsize, int R, int th, int *out) {
   }
 }
 
-static cudaStream_t g_side = nullptr;
+static cudaStream_t g_side = nullptr, g_bigs = nullptr;
 static cudaEvent_t g_fork = nullptr, g_join = nullptr;
 static bool g_big_attr = false;
 
 static int big_stream_fork(cudaStream_t s) {
-  (void)0;
   if (!g_side) {
     LTS_CUDA(cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking));
     LTS_CUDA(cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming));
     LTS_CUDA(cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming));
   }
   if (!g_big_attr) {
-    LTS_CUDA(cudaFuncSetAttribute(k_localize_big<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
-    LTS_CUDA(cudaFuncSetAttribute(k_localize_big<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
+    LTS_CUDA(cudaFuncSetAttribute(k_big_flood<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
+    LTS_CUDA(cudaFuncSetAttribute(k_big_flood<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
     // leave the rest of the unified L1/shared array to L1: the floods re-read
     // region rows and keys that fit there
     int carve = (int)((sizeof(BigSmem) * 100 + 227 * 1024 - 1) / (228 * 1024)) + 1;
-    LTS_CUDA(cudaFuncSetAttribute(k_localize_big<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    LTS_CUDA(cudaFuncSetAttribute(k_localize_big<3>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    LTS_CUDA(cudaFuncSetAttribute(k_big_flood<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    LTS_CUDA(cudaFuncSetAttribute(k_big_flood<3>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     g_big_attr = true;
   }
+  // LTS_BIG_SERIAL (diagnostic): run the large-region floods on the main
+  // stream, alone on the GPU
+  static const bool serial = getenv("LTS_BIG_SERIAL") != nullptr;
+  g_bigs = serial ? s : g_side;
+  if (serial) return 0;
   LTS_CUDA(cudaEventRecord(g_fork, s));
-  LTS_CUDA(cudaStreamWaitEvent(g_side, g_fork, 0));
+  LTS_CUDA(cudaStreamWaitEvent(g_bigs, g_fork, 0));
   return 0;
 }
 
 static int big_stream_join(cudaStream_t s) {
-  LTS_CUDA(cudaEventRecord(g_join, g_side));
+  if (g_bigs == s) return 0;
+  LTS_CUDA(cudaEventRecord(g_join, g_bigs));
   LTS_CUDA(cudaStreamWaitEvent(s, g_join, 0));
+  return 0;
+}
+
+// one flood of every large region still flooding: grid-wide relabelling,
+// one CTA per region for the flood, grid-wide checks, per-region decision
+static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
+  dim3 rg(gx, B.nbig);
+  LTS_CUDA(cudaMemsetAsync(B.nactive, 0, sizeof(int), g_bigs));
+  if (c.g.ndim == 2) {
+    k_big_setup<2><<<rg, 256, 0, g_bigs>>>(A, B);
+    k_big_flood<2><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+    k_big_check<2><<<rg, 256, 0, g_bigs>>>(A, B);
+  } else {
+    k_big_setup<3><<<rg, 256, 0, g_bigs>>>(A, B);
+    k_big_flood<3><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+    k_big_check<3><<<rg, 256, 0, g_bigs>>>(A, B);
+  }
+  k_big_decide<<<NB(B.nbig), 256, 0, g_bigs>>>(A, B);
+  g_launches += 4;
+  LTS_KCHECK();
   return 0;
 }
 
@@ -556,27 +583,25 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     const int nbig = c.h_scal[SC_NBIG];
     const int largest = c.h_scal[SC_LARGEST];
     r.big_regions = nbig;
+    BigArgs B{};
+    int big_gx = 1;
     if (nbig > 0) {
       LTS_TRY(big_stream_fork(s));
-      BigArgs B;
       B.inv = w.binv; B.gbits = w.gbits; B.nrow = w.nrow; B.nrowkey = w.nrowkey; B.qbase = 0; B.nbig = nbig;
       B.queue = w.scal + SC_BIGQ;
       B.v0 = w.bigv0;
-      k_fill_int<<<NB(nbig), 256, 0, g_side>>>(w.bigv0, nbig, 0x7fffffff);
-      {
-        // slot chunks per region: enough blocks for the largest (first) one
-        int gx = (largest + 255) / 256;
-        if (gx > 256) gx = 256;
-        dim3 rg(gx, nbig);
-        if (c.g.ndim == 2) k_big_rows<2><<<rg, 256, 0, g_side>>>(A, B);
-        else k_big_rows<3><<<rg, 256, 0, g_side>>>(A, B);
-        g_launches += 2;
-      }
-      int gb = nbig < 148 ? nbig : 148;
-      if (c.g.ndim == 2) k_localize_big<2><<<gb, BIG_T, sizeof(BigSmem), g_side>>>(A, B);
-      else k_localize_big<3><<<gb, BIG_T, sizeof(BigSmem), g_side>>>(A, B);
-      g_launches++;
-      LTS_KCHECK();
+      B.st = w.bst;
+      B.nactive = w.scal + SC_BIGACT;
+      k_fill_int<<<NB(nbig), 256, 0, g_bigs>>>(w.bigv0, nbig, 0x7fffffff);
+      // slot chunks per region: enough blocks for the largest (first) one
+      big_gx = (largest + 255) / 256;
+      if (big_gx > 256) big_gx = 256;
+      dim3 rg(big_gx, nbig);
+      if (c.g.ndim == 2) k_big_rows<2><<<rg, 256, 0, g_bigs>>>(A, B);
+      else k_big_rows<3><<<rg, 256, 0, g_bigs>>>(A, B);
+      k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B);
+      g_launches += 3;
+      LTS_TRY(big_iteration(c, A, B, big_gx));
     }
     A.qbase = nbig;
     if (R > nbig) {
@@ -612,7 +637,20 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       k_realize<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, g);
       g_launches++;
     }
-    if (nbig > 0) LTS_TRY(big_stream_join(s));
+    if (nbig > 0) {
+      // the remaining floods of the large regions; every other localize-phase
+      // launch is already queued on the main stream
+      for (;;) {
+        LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_BIGACT, w.scal + SC_BIGACT, sizeof(int), cudaMemcpyDeviceToHost, g_bigs));
+        LTS_CUDA(cudaStreamSynchronize(g_bigs));
+        if (c.h_scal[SC_BIGACT] == 0) break;
+        LTS_TRY(big_iteration(c, A, B, big_gx));
+      }
+      dim3 rg(big_gx, nbig);
+      k_big_final<<<rg, 256, 0, g_bigs>>>(A, B);
+      g_launches++;
+      LTS_TRY(big_stream_join(s));
+    }
     k_loc_stats<<<NB(R), 256, 0, s>>>(w.nit, w.st, w.rsize, R, w.scal + SC_STATS);
     g_launches += 1;
     LTS_KCHECK();

@@ -15,10 +15,17 @@ namespace lts {
 namespace rs {
 
 constexpr int RADIX = 256;
-constexpr int THREADS = 512;
+#ifndef LTS_OS_T
+#define LTS_OS_T 512
+#endif
+#ifndef LTS_OS_KPT
+#define LTS_OS_KPT 8
+#endif
+constexpr int THREADS = LTS_OS_T;
 constexpr int WARPS = THREADS / 32;
-constexpr int KPT = 8;
-constexpr int TILE = THREADS * KPT;  // 4096 keys per tile
+constexpr int KPT = LTS_OS_KPT;
+constexpr int TILE = THREADS * KPT;  // 4096 keys per tile by default
+static_assert(THREADS >= RADIX && WARPS <= 32, "one thread per digit");
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_PRE = 2u << 30;
 constexpr uint32_t VAL_MASK = (1u << 30) - 1;
@@ -118,7 +125,7 @@ __global__ void __launch_bounds__(THREADS, LTS_OS_MINB) k_onesweep(
   __shared__ uint16_t s_wh[WARPS][RADIX];
   __shared__ uint32_t s_excl[RADIX];
   __shared__ uint32_t s_start[RADIX];
-  __shared__ uint32_t s_wtot[8];
+  __shared__ uint32_t s_wtot[RADIX / 32];
   __shared__ uint32_t s_hist[RADIX];
   __shared__ uint32_t s_keys[TILE];
   __shared__ uint32_t s_vals[TILE];
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(THREADS, LTS_OS_MINB) k_onesweep(
     if (tid < RADIX) {
       uint32_t off = 0;
 #pragma unroll
-      for (int i = 0; i < 8; i++)
+      for (int i = 0; i < RADIX / 32; i++)
         if (i < warp) off += s_wtot[i];
       s_start[tid] = off + inc - sum;
     }

@@ -23,9 +23,9 @@ torch.cuda.synchronize(); print("pass wall ms", (time.time() - t) * 1e3, pr.repo
 out = np.zeros(256 * 24, np.int64)
 L.lts_debug_big_stats(0, out.ctypes.data_as(ctypes.c_void_p), 256)
 out = out.reshape(256, 24)
-print("k steps cands committed flood_Mcyc check_Mcyc init_Mcyc nit")
+print("k steps cands committed flood_Mcyc nit | per-step cycles: gather probe cut commit")
 for r in out[:12]:
-    print(r[0], r[1], r[2], r[3], round(r[4] / 1e6, 2), round(r[5] / 1e6, 2), round(r[6] / 1e6, 2), r[7],
-          "per-step cyc: climb %d gather %d inv %d probes %d cut %d commit %d insert %d" % tuple((r[8:15] / max(r[1], 1)).astype(int)), "climb-extractions", int(r[15]), "chunk-iters/step %.2f scan %d extract %d climb-steps %d" % (r[16] / max(r[1], 1), r[17] / max(r[16], 1), r[18] / max(r[16], 1), r[19]))
+    st = max(r[1], 1)
+    print(r[0], r[1], r[2], r[3], round(r[4] / 1e6, 2), r[7], "|", *(r[8:12] // st))
 nz = out[out[:, 0] > 0]
 print("regions", len(nz), "sum flood Mcyc", nz[:, 4].sum() / 1e6, "max", nz[:, 4].max() / 1e6)
