@@ -61,7 +61,8 @@ enum { BST_T = 0, BST_ACTIVE, BST_FIN, BST_STATUS, BST_BAD, BST_DIFF, BST_W = 8 
 
 // optional per-region instrumentation (lts_debug_big_stats): big-queue slot i
 // records [k, steps, candidates, committed, flood cycles, -, -, n_iters,
-// gather, probe, cut, commit cycles]
+// gather, probe, cut, commit cycles, steps with j <= 8, j <= 32,
+// sum ceil(j/32), unpreempted steps, sum ceil(j/64)]
 constexpr int DBG_MAX = 256, DBG_W = 24;
 __device__ long long d_dbg[DBG_MAX * DBG_W];
 __device__ int d_dbg_on;
@@ -297,6 +298,13 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     e += j;
     nst++;
     ncand += nc;
+    if (dbg && tid == 0) {  // commit-size histogram (lts_debug_big_stats)
+      dbg[12] += j <= 8;
+      dbg[13] += j <= 32;
+      dbg[14] += (j + 31) / 32;
+      dbg[15] += j == nc;
+      dbg[16] += (j + 63) / 64;
+    }
     __syncthreads();
     if (tid == 0) S.cut = 0x7fffffff;
     BIG_TICK(tm)

@@ -16,15 +16,15 @@ namespace rs {
 
 constexpr int RADIX = 256;
 #ifndef LTS_OS_T
-#define LTS_OS_T 512
+#define LTS_OS_T 256
 #endif
 #ifndef LTS_OS_KPT
-#define LTS_OS_KPT 8
+#define LTS_OS_KPT 16
 #endif
 constexpr int THREADS = LTS_OS_T;
 constexpr int WARPS = THREADS / 32;
 constexpr int KPT = LTS_OS_KPT;
-constexpr int TILE = THREADS * KPT;  // 4096 keys per tile by default
+constexpr int TILE = THREADS * KPT;  // 4096 keys per tile (256 threads x 16, 4 CTAs per SM)
 static_assert(THREADS >= RADIX && WARPS <= 32, "one thread per digit");
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_PRE = 2u << 30;
@@ -114,7 +114,7 @@ __device__ long long d_sort_dbg[8];
 __device__ int d_sort_dbg_on;
 
 #ifndef LTS_OS_MINB
-#define LTS_OS_MINB 1
+#define LTS_OS_MINB 4
 #endif
 template <bool FLOATKEY, bool HAS_VALS, bool WRITE_KEYS, bool WRITE_RANK>
 __global__ void __launch_bounds__(THREADS, LTS_OS_MINB) k_onesweep(

@@ -26,6 +26,7 @@ out = out.reshape(256, 24)
 print("k steps cands committed flood_Mcyc nit | per-step cycles: gather probe cut commit")
 for r in out[:12]:
     st = max(r[1], 1)
-    print(r[0], r[1], r[2], r[3], round(r[4] / 1e6, 2), r[7], "|", *(r[8:12] // st))
+    print(r[0], r[1], r[2], r[3], round(r[4] / 1e6, 2), r[7], "|", *(r[8:12] // st),
+          "| j<=8:", r[12], "j<=32:", r[13], "sum ceil(j/32):", r[14], "unpreempted:", r[15], "sum ceil(j/64):", r[16])
 nz = out[out[:, 0] > 0]
 print("regions", len(nz), "sum flood Mcyc", nz[:, 4].sum() / 1e6, "max", nz[:, 4].max() / 1e6)
