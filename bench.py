@@ -260,7 +260,6 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp))
-    dom = max((k for k in phases if k != "total"), key=lambda k: phases[k])
     kernels = {
         "order_sort": {"ms": sort_ms, "bytes_per_voxel": 64, "achieved_gbs": sort_gbs,
                        "frac": sort_gbs / hbm, "traffic": traffic.get("order_sort")},
@@ -268,18 +267,28 @@ def main():
                      "frac": cls_gbs / hbm, "traffic": traffic.get("classify")},
         "classify_ascent": {"ms": clsptr_ms, "bytes_per_voxel": 9,
                             "achieved_gbs": 9.0 * n / (clsptr_ms * 1e-3) / 1e9,
-                            "frac": 9.0 * n / (clsptr_ms * 1e-3) / 1e9 / hbm},
+                            "frac": 9.0 * n / (clsptr_ms * 1e-3) / 1e9 / hbm,
+                            "traffic": traffic.get("classify_ascent")},
     }
-    # dominant phase: latency-bound floods / union-find; its algorithmic bytes
-    # are the region data it must touch
-    claimed = sum(p.claimed for p in report.passes)
-    dom_bytes = {"localize": 76.0 * claimed, "discover": 60.0 * n * 2, "order": 64.0 * n,
-                 "classify": 5.0 * n * 6, "integrate": 24.0 * n * 2, "assemble": 28.0 * n * 2,
-                 "realize": 12.0 * claimed, "verify": 6.0 * n}.get(dom, 0.0)
-    dom_gbs = dom_bytes / (phases[dom] * 1e-3) / 1e9 if phases[dom] > 0 else 0.0
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": hbm, "unit": "GB/s",
-                "frac": dom_gbs / hbm, "traffic": traffic.get(dom), "peak_source": peak_kind,
-                "share_of_step": phases[dom] / phases["total"] if phases["total"] else None}
+    # dominant kernel: the large-region flood (k_big_flood), timed by the
+    # library with CUDA events on the stream it runs on.  Algorithmic bytes per
+    # flooded region slot: its neighbour-key row (4 K B), its key -> index
+    # entry (4 B) and its label (4 B); DESIGN.md section 4.
+    K = 14 if mesh.dim == 3 else 6
+    flood_ms = float(rep.phase_ms[9])
+    flood_launches = int(rep.phase_ms[N.PH_FLOOD_LAUNCHES])
+    flood_slots = float(rep.phase_ms[N.PH_FLOOD_SLOTS])
+    per_launch_ms = flood_ms / max(flood_launches, 1)
+    flood_bytes = (4.0 * K + 8.0) * flood_slots / max(flood_launches, 1)
+    flood_gbs = flood_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": "k_big_flood", "achieved": flood_gbs, "peak": hbm,
+                "unit": "GB/s", "frac": flood_gbs / hbm, "traffic": traffic.get("k_big_flood"),
+                "peak_source": peak_kind, "launches": flood_launches, "ms_per_launch": per_launch_ms,
+                "bytes_per_launch": flood_bytes,
+                "share_of_step": flood_ms / phases["total"] if phases["total"] else None,
+                "slots_per_s": flood_slots / (flood_ms * 1e-3) if flood_ms > 0 else None,
+                "note": "latency-bound priority floods (one CTA per region, about one L2 round "
+                        "trip and five barriers per batched step); DESIGN.md section 4"}
 
     # ---- end to end through the public API with host buffers ---------------
     g_host = torch.empty(n, dtype=torch.float32).pin_memory()

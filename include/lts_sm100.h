@@ -54,6 +54,9 @@ extern "C" {
 #define LTS_PH_REALIZE 6    /* A13: saddle-value gathers                     */
 #define LTS_PH_VERIFY 7     /* A11/A12: restore + verify                     */
 #define LTS_PH_TOTAL 8
+#define LTS_PH_FLOOD_KERNEL 9    /* device time of the large-region flood kernel  */
+#define LTS_PH_FLOOD_LAUNCHES 10 /* its launch count (a count, not ms)           */
+#define LTS_PH_FLOOD_SLOTS 11    /* region slots it flooded, summed over launches */
 
 typedef struct {
   int32_t max_iterations;           /* SPEC.md:303 maxIterations (default 100)  */

@@ -28,7 +28,8 @@ E_INVALID = 9
 MAX_REPORT_PASSES = 64
 NUM_PHASES = 12
 PHASES = ["order", "classify", "discover", "assemble", "localize", "integrate", "realize",
-          "verify", "total"]
+          "verify", "total", "flood_kernel"]
+PH_FLOOD_LAUNCHES, PH_FLOOD_SLOTS = 10, 11  # counts reported in phase_ms slots
 
 
 class lts_options_t(ctypes.Structure):

@@ -53,6 +53,7 @@ struct BigArgs {
   int *queue;
   int *st;           // per big region: BST_W ints of flood state (below)
   int *nactive;      // regions still flooding after the last decide
+  unsigned long long *work;  // sum of the region sizes flooded (report)
 };
 
 // per-region flood state, kept in global memory between the grid-wide
@@ -480,6 +481,7 @@ __global__ void __launch_bounds__(BIG_T) k_big_flood(LocArgs A, BigArgs Bg) {
   const int qa = Bg.qbase + qi;  // absolute big-queue position
   long long *dbg = (d_dbg_on && qa < DBG_MAX) ? d_dbg + qa * DBG_W : nullptr;
   if (dbg && tid == 0) dbg[0] = k;
+  if (tid == 0) atomicAdd(Bg.work, (unsigned long long)k);
   const long long c0 = clock64();
   big_flood<K>(S, G, t & 1, big_buf(A, t) + lo, big_buf(A, t + 1) + lo, dbg);
   if (dbg && tid == 0) dbg[4] += clock64() - c0;

@@ -205,6 +205,7 @@ enum {
   SC_BIGQ = 30,
   SC_LARGEST = 31,
   SC_BIGACT = 32,
+  SC_BIGWORK = 34,  // 2 ints: 64-bit sum of region sizes flooded by k_big_flood
   SC_N = 64
 };
 
@@ -269,6 +270,7 @@ struct Ctx {
   int *h_scal;  // pinned
   bool timing;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  int64_t flood_launches = 0, flood_slots = 0;
 };
 
 static int *g_h_scal = nullptr;
@@ -415,13 +417,25 @@ static int big_stream_join(cudaStream_t s) {
 static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
   dim3 rg(gx, B.nbig);
   LTS_CUDA(cudaMemsetAsync(B.nactive, 0, sizeof(int), g_bigs));
+  if (c.g.ndim == 2) k_big_setup<2><<<rg, 256, 0, g_bigs>>>(A, B);
+  else k_big_setup<3><<<rg, 256, 0, g_bigs>>>(A, B);
+  // device time of the flood kernel itself (report slot LTS_PH_FLOOD_KERNEL)
+  cudaEvent_t fa = nullptr, fb = nullptr;
+  if (c.timing) {
+    fa = next_event();
+    LTS_CUDA(cudaEventRecord(fa, g_bigs));
+  }
+  if (c.g.ndim == 2) k_big_flood<2><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+  else k_big_flood<3><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+  if (c.timing) {
+    fb = next_event();
+    LTS_CUDA(cudaEventRecord(fb, g_bigs));
+    c.marks.push_back({LTS_PH_FLOOD_KERNEL, {fa, fb}});
+    c.flood_launches++;
+  }
   if (c.g.ndim == 2) {
-    k_big_setup<2><<<rg, 256, 0, g_bigs>>>(A, B);
-    k_big_flood<2><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
     k_big_check<2><<<rg, 256, 0, g_bigs>>>(A, B);
   } else {
-    k_big_setup<3><<<rg, 256, 0, g_bigs>>>(A, B);
-    k_big_flood<3><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
     k_big_check<3><<<rg, 256, 0, g_bigs>>>(A, B);
   }
   k_big_decide<<<NB(B.nbig), 256, 0, g_bigs>>>(A, B);
@@ -592,6 +606,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       B.v0 = w.bigv0;
       B.st = w.bst;
       B.nactive = w.scal + SC_BIGACT;
+      B.work = reinterpret_cast<unsigned long long *>(w.scal + SC_BIGWORK);
       k_fill_int<<<NB(nbig), 256, 0, g_bigs>>>(w.bigv0, nbig, 0x7fffffff);
       // slot chunks per region: enough blocks for the largest (first) one
       big_gx = (largest + 255) / 256;
@@ -641,9 +656,12 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       // the remaining floods of the large regions; every other localize-phase
       // launch is already queued on the main stream
       for (;;) {
-        LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_BIGACT, w.scal + SC_BIGACT, sizeof(int), cudaMemcpyDeviceToHost, g_bigs));
+        LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_BIGACT, w.scal + SC_BIGACT, 4 * sizeof(int), cudaMemcpyDeviceToHost, g_bigs));
         LTS_CUDA(cudaStreamSynchronize(g_bigs));
-        if (c.h_scal[SC_BIGACT] == 0) break;
+        if (c.h_scal[SC_BIGACT] == 0) {
+          c.flood_slots += *reinterpret_cast<const long long *>(c.h_scal + SC_BIGWORK);
+          break;
+        }
         LTS_TRY(big_iteration(c, A, B, big_gx));
       }
       dim3 rg(big_gx, nbig);
@@ -976,6 +994,8 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
     float tot = 0;
     cudaEventElapsedTime(&tot, t0, t1);
     R.phase_ms[LTS_PH_TOTAL] = tot;
+    R.phase_ms[LTS_PH_FLOOD_LAUNCHES] = (double)c.flood_launches;
+    R.phase_ms[LTS_PH_FLOOD_SLOTS] = (double)c.flood_slots;
   }
   if (rep) *rep = R;
   if (!ok) return lts_set_error(LTS_E_VERIFY_FAILED_AT_CAP, "verify_constraints still failing after maxIterations outer iterations");
