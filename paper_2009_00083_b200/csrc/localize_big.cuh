@@ -54,7 +54,20 @@ struct BigArgs {
   int *st;           // per big region: BST_W ints of flood state (below)
   int *nactive;      // regions still flooding after the last decide
   unsigned long long *work;  // sum of the region sizes flooded (report)
+  const int *bpre;   // nbig + 1: exclusive prefix of the big-region sizes (queue order)
+  int bslots;        // bpre[nbig]: slots of all big regions
 };
+
+// big-queue index of flat big-region slot i (largest qi with bpre[qi] <= i)
+__device__ __forceinline__ int big_locate(const BigArgs &Bg, int i) {
+  int lo = 0, hi = Bg.nbig - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (Bg.bpre[mid] <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
 
 // per-region flood state, kept in global memory between the grid-wide
 // setup / check kernels and the one-CTA-per-region flood kernel
@@ -328,31 +341,70 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_big_rows(LocArgs A, BigArgs Bg) {
   constexpr int K = NDIM == 2 ? 6 : 14;
-  const int qi = blockIdx.y;
-  const int rid = A.order[Bg.qbase + qi];
-  const int lo = A.rptr[rid];
-  const int k = A.rptr[rid + 1] - lo;
   const int n = (int)A.g.n;
-  const int s = A.verts[lo];
-  const int srank = eff_rank(A.rank, s, A.rev, n);
-  int mine = 0x7fffffff;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < k; p += gridDim.x * blockDim.x) {
-    int x, y, z;
-    coords(A.g, A.verts[lo + p], x, y, z);
-    bool out = false;
-    int *row = Bg.nrow + ((size_t)lo + p) * K;
+  const int lane = threadIdx.x & 31;
+  // flat over the slots of all big regions; warps stay converged so the
+  // per-region minimum is reduced over the lanes of the same region
+  for (int b0 = blockIdx.x * blockDim.x; b0 < Bg.bslots; b0 += gridDim.x * blockDim.x) {
+    const int i = b0 + threadIdx.x;
+    const int qi = i < Bg.bslots ? big_locate(Bg, i) : -1;
+    int mine = 0x7fffffff;
+    if (qi >= 0) {
+      const int rid = A.order[Bg.qbase + qi];
+      const int lo = A.rptr[rid];
+      const int p = i - Bg.bpre[qi];
+      const int s = A.verts[lo];
+      const int srank = eff_rank(A.rank, s, A.rev, n);
+      int x, y, z;
+      coords(A.g, A.verts[lo + p], x, y, z);
+      bool out = false;
+      int *row = Bg.nrow + ((size_t)lo + p) * K;
 #pragma unroll
-    for (int kk = 0; kk < K; kk++) {
-      int u = nbr_at(A.g, x, y, z, kk);
-      row[kk] = member(A, u, rid, s);
-      if (p >= 1 && u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) out = true;
+      for (int kk = 0; kk < K; kk++) {
+        int u = nbr_at(A.g, x, y, z, kk);
+        row[kk] = member(A, u, rid, s);
+        if (p >= 1 && u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) out = true;
+      }
+      A.sfl[lo + p] = out ? SF_OUT : 0;
+      if (out) mine = p;
+      A.buf0[lo + p] = p;
     }
-    A.sfl[lo + p] = out ? SF_OUT : 0;
-    if (out && p < mine) mine = p;
-    A.buf0[lo + p] = p;
+    const unsigned peers = __match_any_sync(0xffffffffu, qi);
+    const int m = __reduce_min_sync(peers, mine);
+    if (qi >= 0 && lane == __ffs(peers) - 1 && m != 0x7fffffff) atomicMin(Bg.v0 + qi, m);
   }
-  mine = __reduce_min_sync(0xffffffffu, mine);
-  if ((threadIdx.x & 31) == 0 && mine != 0x7fffffff) atomicMin(Bg.v0 + qi, mine);
+}
+
+// exclusive prefix of the big-region sizes in queue order (one block)
+__global__ void __launch_bounds__(1024) k_big_prefix(LocArgs A, BigArgs Bg, int *bpre) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < Bg.nbig; b0 += 1024) {
+    const int qi = b0 + threadIdx.x;
+    int x = 0;
+    if (qi < Bg.nbig) {
+      const int rid = A.order[Bg.qbase + qi];
+      x = A.rptr[rid + 1] - A.rptr[rid];
+    }
+    int inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    int pre = carry;
+    for (int w = 0; w < warp; w++) pre += wsum[w];
+    if (qi < Bg.nbig) bpre[qi] = pre + inc - x;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = pre + inc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bpre[Bg.nbig] = carry;
 }
 
 // The big-region floods run as an iteration of four launches over all large
@@ -406,27 +458,25 @@ __global__ void k_big_init(LocArgs A, BigArgs Bg) {
   }
 }
 
-// grid (chunks, regions): inverse and neighbour keys of the next flood.  One
-// row per thread, the K label gathers of a row independent of each other.
+// flat over big-region slots: inverse and neighbour keys of the next flood.
+// One row per thread, the K label gathers of a row independent of each other.
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_big_setup(LocArgs A, BigArgs Bg) {
   constexpr int K = NDIM == 2 ? 6 : 14;
   static_assert(K % 2 == 0, "rows are read and written as int2");
-  const int qi = blockIdx.y;
-  const int *st = Bg.st + qi * BST_W;
-  if (!st[BST_ACTIVE]) return;
-  const int t = st[BST_T];
-  const bool asc = t & 1;
-  const BigRef R = big_ref(A, Bg, qi);
-  const int k = R.k;
-  const int *cin = big_buf(A, t) + R.lo;
-  int *inv = Bg.inv + R.lo + R.rid;
-  int *krow = Bg.nrowkey + ((size_t)R.lo + R.rid) * K;
-  const int *rows = Bg.nrow + (size_t)R.lo * K;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < k; p += gridDim.x * blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Bg.bslots; i += gridDim.x * blockDim.x) {
+    const int qi = big_locate(Bg, i);
+    const int *st = Bg.st + qi * BST_W;
+    if (!st[BST_ACTIVE]) continue;
+    const int t = st[BST_T];
+    const bool asc = t & 1;
+    const BigRef R = big_ref(A, Bg, qi);
+    const int k = R.k;
+    const int p = i - Bg.bpre[qi];
+    const int *cin = big_buf(A, t) + R.lo;
     const int kp = flood_key(cin[p], asc, k);
-    inv[kp] = p;
-    const int2 *row = reinterpret_cast<const int2 *>(rows + (size_t)p * K);
+    Bg.inv[R.lo + R.rid + kp] = p;
+    const int2 *row = reinterpret_cast<const int2 *>(Bg.nrow + ((size_t)R.lo + p) * K);
     int q[K], c[K];
 #pragma unroll
     for (int h = 0; h < K / 2; h++) {
@@ -436,7 +486,7 @@ __global__ void __launch_bounds__(256) k_big_setup(LocArgs A, BigArgs Bg) {
     }
 #pragma unroll
     for (int kk = 0; kk < K; kk++) c[kk] = q[kk] >= 0 ? cin[q[kk]] : 0;
-    int2 *dst = reinterpret_cast<int2 *>(krow + (size_t)kp * K);
+    int2 *dst = reinterpret_cast<int2 *>(Bg.nrowkey + ((size_t)R.lo + R.rid + kp) * K);
 #pragma unroll
     for (int h = 0; h < K / 2; h++)
       dst[h] = make_int2(q[2 * h] >= 0 ? flood_key(c[2 * h], asc, k) : -1,
@@ -487,54 +537,60 @@ __global__ void __launch_bounds__(BIG_T) k_big_flood(LocArgs A, BigArgs Bg) {
   if (dbg && tid == 0) dbg[4] += clock64() - c0;
 }
 
-// grid (chunks, regions): constraint check of state t+1 (desc flood: local
+// flat over big-region slots: constraint check of state t+1 (desc flood: local
 // minima get SF_MIN, unauthorized if not SF_OUT; asc flood: any local maximum
 // besides the saddle) and, from t+1 >= 3 on, state t+1 != state t-1
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_big_check(LocArgs A, BigArgs Bg) {
   constexpr int K = NDIM == 2 ? 6 : 14;
-  const int qi = blockIdx.y;
-  int *st = Bg.st + qi * BST_W;
-  if (!st[BST_ACTIVE]) return;
-  const int t1 = st[BST_T] + 1;
-  const bool desc = (t1 & 1) == 1;  // flood t1-1 was descending
-  const BigRef R = big_ref(A, Bg, qi);
-  const int *cur = big_buf(A, t1) + R.lo;
-  const int *old = big_buf(A, t1 + 1) + R.lo;  // state t1-2
-  const int *rows = Bg.nrow + (size_t)R.lo * K;
-  uint8_t *sfl = A.sfl + R.lo;
-  bool bad = false, diff = false;
-  for (int p = 1 + blockIdx.x * blockDim.x + threadIdx.x; p < R.k; p += gridDim.x * blockDim.x) {
-    const int2 *row = reinterpret_cast<const int2 *>(rows + (size_t)p * K);
-    const int c = cur[p];
-    int q[K];
+  const int lane = threadIdx.x & 31;
+  for (int b0 = blockIdx.x * blockDim.x; b0 < Bg.bslots; b0 += gridDim.x * blockDim.x) {
+    const int i = b0 + threadIdx.x;
+    int qi = i < Bg.bslots ? big_locate(Bg, i) : -1;
+    int *st = qi >= 0 ? Bg.st + qi * BST_W : nullptr;
+    if (st && !st[BST_ACTIVE]) qi = -1;
+    bool bad = false, diff = false;
+    if (qi >= 0) {
+      const int t1 = st[BST_T] + 1;
+      const bool desc = (t1 & 1) == 1;  // flood t1-1 was descending
+      const BigRef R = big_ref(A, Bg, qi);
+      const int p = i - Bg.bpre[qi];
+      const int *cur = big_buf(A, t1) + R.lo;
+      const int *old = big_buf(A, t1 + 1) + R.lo;  // state t1-2
+      const int c = cur[p];
+      if (t1 >= 3 && c != old[p]) diff = true;
+      if (p >= 1) {
+        const int2 *row = reinterpret_cast<const int2 *>(Bg.nrow + ((size_t)R.lo + p) * K);
+        int q[K];
 #pragma unroll
-    for (int h = 0; h < K / 2; h++) {
-      const int2 v = row[h];
-      q[2 * h] = v.x;
-      q[2 * h + 1] = v.y;
-    }
-    bool ext = true;
+        for (int h = 0; h < K / 2; h++) {
+          const int2 v = row[h];
+          q[2 * h] = v.x;
+          q[2 * h + 1] = v.y;
+        }
+        bool ext = true;
 #pragma unroll
-    for (int kk = 0; kk < K; kk++)
-      if (q[kk] >= 0 && (desc ? cur[q[kk]] < c : cur[q[kk]] > c)) ext = false;
-    if (desc) {
-      uint8_t f = sfl[p];
-      f = ext ? (f | SF_MIN) : (f & (uint8_t)~SF_MIN);
-      sfl[p] = f;
-      if (ext && !(f & SF_OUT)) bad = true;
-    } else if (ext) {
-      bad = true;
+        for (int kk = 0; kk < K; kk++)
+          if (q[kk] >= 0 && (desc ? cur[q[kk]] < c : cur[q[kk]] > c)) ext = false;
+        if (desc) {
+          uint8_t *sfl = A.sfl + R.lo;
+          uint8_t f = sfl[p];
+          f = ext ? (f | SF_MIN) : (f & (uint8_t)~SF_MIN);
+          sfl[p] = f;
+          if (ext && !(f & SF_OUT)) bad = true;
+        } else if (ext) {
+          bad = true;
+        }
+      }
     }
-    if (t1 >= 3 && c != old[p]) diff = true;
-  }
-  // p = 0 (the saddle) takes part only in the cycle comparison
-  if (t1 >= 3 && blockIdx.x == 0 && threadIdx.x == 0 && cur[0] != old[0]) diff = true;
-  bad = __any_sync(0xffffffffu, bad);
-  diff = __any_sync(0xffffffffu, diff);
-  if ((threadIdx.x & 31) == 0) {
-    if (bad) atomicOr(st + BST_BAD, 1);
-    if (diff) atomicOr(st + BST_DIFF, 1);
+    // one atomic per region and warp
+    const unsigned peers = __match_any_sync(0xffffffffu, qi);
+    const unsigned bb = __ballot_sync(0xffffffffu, bad) & peers;
+    const unsigned dd = __ballot_sync(0xffffffffu, diff) & peers;
+    if (qi >= 0 && lane == __ffs(peers) - 1) {
+      if (bb) atomicOr(st + BST_BAD, 1);
+      if (dd) atomicOr(st + BST_DIFF, 1);
+    }
   }
 }
 
@@ -567,20 +623,21 @@ __global__ void k_big_decide(LocArgs A, BigArgs Bg) {
   }
 }
 
-// grid (chunks, regions): final local order, status and flood count
+// flat over big-region slots: final local order, status and flood count
 __global__ void __launch_bounds__(256) k_big_final(LocArgs A, BigArgs Bg) {
-  const int qi = blockIdx.y;
-  const int *st = Bg.st + qi * BST_W;
-  const BigRef R = big_ref(A, Bg, qi);
-  const int fin = st[BST_FIN];
-  const int *fb = fin >= 0 ? big_buf(A, fin) + R.lo : nullptr;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < R.k; p += gridDim.x * blockDim.x)
-    A.out[R.lo + p] = fb ? fb[p] : p;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    A.status[R.rid] = st[BST_STATUS];
-    A.n_iters[R.rid] = st[BST_T];
-    const int qa = Bg.qbase + qi;
-    if (d_dbg_on && qa < DBG_MAX) d_dbg[qa * DBG_W + 7] = st[BST_T];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Bg.bslots; i += gridDim.x * blockDim.x) {
+    const int qi = big_locate(Bg, i);
+    const int *st = Bg.st + qi * BST_W;
+    const BigRef R = big_ref(A, Bg, qi);
+    const int p = i - Bg.bpre[qi];
+    const int fin = st[BST_FIN];
+    A.out[R.lo + p] = fin >= 0 ? big_buf(A, fin)[R.lo + p] : p;
+    if (p == 0) {
+      A.status[R.rid] = st[BST_STATUS];
+      A.n_iters[R.rid] = st[BST_T];
+      const int qa = Bg.qbase + qi;
+      if (d_dbg_on && qa < DBG_MAX) d_dbg[qa * DBG_W + 7] = st[BST_T];
+    }
   }
 }
 

@@ -176,7 +176,7 @@ struct WS {
   int *verts, *buf0, *buf1, *buf2, *out;
   unsigned long long *gheap;
   uint8_t *sfl;
-  int *binv, *nrow, *nrowkey, *bigv0, *bst;
+  int *binv, *nrow, *nrowkey, *bigv0, *bst, *bpre;
   uint32_t *cbits;
   uint32_t *gbits;
   rs::Bufs sb;
@@ -206,6 +206,7 @@ enum {
   SC_LARGEST = 31,
   SC_BIGACT = 32,
   SC_BIGWORK = 34,  // 2 ints: 64-bit sum of region sizes flooded by k_big_flood
+  SC_BIGSLOTS = 36, // = SC_NBIG + 7: slots of the big regions
   SC_N = 64
 };
 
@@ -243,6 +244,7 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->binv = i32(3 * n + 8);
   w->bigv0 = i32(n1);
   w->bst = i32(BST_W * (n1 / BIG_THRESHOLD + 2));  // regions with k > BIG_THRESHOLD
+  w->bpre = i32(n1 / BIG_THRESHOLD + 4);
   w->cbits = u32(n / 32 + 64);
   w->gbits = u32(6 * n + 64);
   w->nrow = i32((ndim == 2 ? 6 : 14) * s2);
@@ -368,9 +370,13 @@ __global__ void k_loc_stats(const int *nit, const int *st, const int *rsize, int
 
 // out[0] = regions with k > th, out[2] = largest k (saddle included)
 // out[0] = #regions with k > th, out[2] = largest k
+// out[7] = slots of the regions with k > th
 __global__ void k_count_big(const int *rsize, int R, int th, int *out) {
   GRID_STRIDE(r, R) {
-    if (rsize[r] + 1 > th) atomicAdd(out, 1);
+    if (rsize[r] + 1 > th) {
+      atomicAdd(out, 1);
+      atomicAdd(out + 7, rsize[r] + 1);
+    }
     atomicMax(out + 2, rsize[r] + 1);
   }
 }
@@ -415,7 +421,7 @@ static int big_stream_join(cudaStream_t s) {
 // one flood of every large region still flooding: grid-wide relabelling,
 // one CTA per region for the flood, grid-wide checks, per-region decision
 static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
-  dim3 rg(gx, B.nbig);
+  const int rg = gx;
   LTS_CUDA(cudaMemsetAsync(B.nactive, 0, sizeof(int), g_bigs));
   if (c.g.ndim == 2) k_big_setup<2><<<rg, 256, 0, g_bigs>>>(A, B);
   else k_big_setup<3><<<rg, 256, 0, g_bigs>>>(A, B);
@@ -593,9 +599,8 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     // to the CTA-batched flood on a side stream, the rest to warp floods
     k_count_big<<<NB(R), 256, 0, s>>>(w.rsize, R, BIG_THRESHOLD, w.scal + SC_NBIG);
     g_launches++;
-    LTS_TRY(readback(c, SC_NBIG, 3));
+    LTS_TRY(readback(c, SC_NBIG, 8));
     const int nbig = c.h_scal[SC_NBIG];
-    const int largest = c.h_scal[SC_LARGEST];
     r.big_regions = nbig;
     BigArgs B{};
     int big_gx = 1;
@@ -608,14 +613,15 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       B.nactive = w.scal + SC_BIGACT;
       B.work = reinterpret_cast<unsigned long long *>(w.scal + SC_BIGWORK);
       k_fill_int<<<NB(nbig), 256, 0, g_bigs>>>(w.bigv0, nbig, 0x7fffffff);
-      // slot chunks per region: enough blocks for the largest (first) one
-      big_gx = (largest + 255) / 256;
-      if (big_gx > 256) big_gx = 256;
-      dim3 rg(big_gx, nbig);
-      if (c.g.ndim == 2) k_big_rows<2><<<rg, 256, 0, g_bigs>>>(A, B);
-      else k_big_rows<3><<<rg, 256, 0, g_bigs>>>(A, B);
+      k_big_prefix<<<1, 1024, 0, g_bigs>>>(A, B, w.bpre);
+      B.bpre = w.bpre;
+      B.bslots = c.h_scal[SC_BIGSLOTS];
+      // flat kernels over all big-region slots
+      big_gx = (int)std::min<int64_t>((B.bslots + 255) / 256, 148 * 8);
+      if (c.g.ndim == 2) k_big_rows<2><<<big_gx, 256, 0, g_bigs>>>(A, B);
+      else k_big_rows<3><<<big_gx, 256, 0, g_bigs>>>(A, B);
       k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B);
-      g_launches += 3;
+      g_launches += 4;
       LTS_TRY(big_iteration(c, A, B, big_gx));
     }
     A.qbase = nbig;
@@ -664,8 +670,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         }
         LTS_TRY(big_iteration(c, A, B, big_gx));
       }
-      dim3 rg(big_gx, nbig);
-      k_big_final<<<rg, 256, 0, g_bigs>>>(A, B);
+      k_big_final<<<big_gx, 256, 0, g_bigs>>>(A, B);
       g_launches++;
       LTS_TRY(big_stream_join(s));
     }
