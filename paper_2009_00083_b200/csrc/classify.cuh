@@ -10,11 +10,15 @@
 // table (triangulation.py:52-78 -- over-connected):
 // lower = LUT[valid & ~upper], upper = LUT[upper].
 //
-// Memory layout: a CTA owns a 32 x 8 (x, y) column of the grid and marches in
-// z; three (8+2) x (32+2) rank planes with halo live in shared memory, so each
-// rank is read from HBM about 1.3 times (halo) and every output is written
+// Memory layout: a CTA owns a 32 x 32 (x, y) column of the grid and marches in
+// z; a ring of (32+2) x (32+4) rank planes with halo lives in shared memory, so
+// each rank is read from HBM once (halos hit L2) and every output is written
 // once, coalesced.  No integer division: coordinates come from the launch grid.
+// 3-D grids with nx % 4 == 0 take the TMA-fed register-marching kernel of
+// classify_zreg.cuh instead (flags / pointer variants).
 #pragma once
+#include <cstdlib>
+
 #include "lts_common.cuh"
 
 namespace lts {
@@ -319,9 +323,13 @@ __global__ void __launch_bounds__(CP_TX *CP_TY) k_classify_tile(Grid g, const in
   }
 }
 
+inline bool launch_classify_zreg(const Grid &g, const int32_t *rank, uint8_t *flags, int32_t *ptr, int ptr_kind,
+                                 cudaStream_t s);
+
 inline void launch_classify(const Grid &g, const int32_t *rank, uint8_t *flags, int16_t *lower,
                             int16_t *upper, const uint8_t *lut, int32_t *ptr, int ptr_kind,
                             cudaStream_t s) {
+  if (lower == nullptr && launch_classify_zreg(g, rank, flags, ptr, ptr_kind, s)) return;
   dim3 blk(CP_TX, CP_TY);
   dim3 grd((g.nx + CP_W - 1) / CP_W, (g.ny + CP_TY * CP_RY - 1) / (CP_TY * CP_RY),
            g.ndim == 2 ? 1 : (g.nz + CP_ZC - 1) / CP_ZC);

@@ -21,6 +21,7 @@
 #include "prims.cuh"
 #include "sort.cuh"
 #include "classify.cuh"
+#include "classify_zreg.cuh"
 #include "discover.cuh"
 #include "localize.cuh"
 #include "localize_big.cuh"

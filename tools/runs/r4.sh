@@ -1,0 +1,2 @@
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+for c in 3 5; do python tools/kbench.py $c; LTS_SM100_LIB=var/lib_minb2.so python tools/kbench.py $c; done
