@@ -9,6 +9,9 @@
 // memory so global writes are digit-contiguous.  Tiles are claimed from an
 // atomic counter so look-back always waits on resident blocks.
 #pragma once
+#include <algorithm>
+#include <cstdlib>
+
 #include "lts_common.cuh"
 
 namespace lts {
@@ -284,6 +287,107 @@ __global__ void __launch_bounds__(THREADS, LTS_OS_MINB) k_onesweep(
 #undef SORT_TICK
 }
 
+// ---------------------------------------------------------------------------
+// rank[id] = position, from the sorted ids (inverse), without a random 4-byte
+// scatter over the whole rank array: (1) the inverse is partitioned into RB
+// buckets by id high bits (bucket b = ids [b*W, (b+1)*W): exactly W entries,
+// so each bucket's region is known), staged through shared memory so every
+// tile writes one contiguous run per bucket; (2) the pairs are placed bucket
+// after bucket, so the rank window being written (n/RB ids) stays in L2 and
+// leaves it as full lines.
+// ---------------------------------------------------------------------------
+#ifndef LTS_RB_BITS
+#define LTS_RB_BITS 6
+#endif
+constexpr int RB_BITS = LTS_RB_BITS, RB = 1 << RB_BITS;
+
+__global__ void __launch_bounds__(THREADS) k_rank_bucket(const uint32_t *__restrict__ inv, int64_t n, int bshift,
+                                                        uint32_t *__restrict__ pos_out,
+                                                        uint32_t *__restrict__ id_out, uint32_t *ctr) {
+  __shared__ uint32_t s_pos[TILE], s_id[TILE];
+  __shared__ uint32_t s_wc[WARPS][RB];
+  static_assert(RB <= 64 && WARPS * RB <= 2 * THREADS, "bucket counters");
+  __shared__ uint32_t s_start[RB], s_base[RB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (n + TILE - 1) / TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * TILE;
+    for (int i = tid; i < WARPS * RB; i += THREADS) (&s_wc[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t id[KPT], r[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      const int64_t idx = base + warp * 32 * KPT + j * 32 + lane;
+      id[j] = idx < n ? inv[idx] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      const bool ok = id[j] != 0xffffffffu;
+      const uint32_t b = ok ? (id[j] >> bshift) : 0u;
+      unsigned peers = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+      for (int t = 0; t < RB_BITS; t++) {
+        const unsigned bal = __ballot_sync(0xffffffffu, (b >> t) & 1u);
+        peers &= ((b >> t) & 1u) ? bal : ~bal;
+      }
+      const int leader = __ffs(peers) - 1;
+      uint32_t cnt = 0;
+      if (ok && lane == leader) {
+        cnt = s_wc[warp][b];
+        s_wc[warp][b] = cnt + __popc(peers);
+      }
+      cnt = __shfl_sync(0xffffffffu, cnt, leader < 0 ? 0 : leader);
+      r[j] = cnt + __popc(peers & lanemask_lt());
+      __syncwarp();
+    }
+    __syncthreads();
+    __shared__ uint32_t s_half;
+    uint32_t sum = 0, inc = 0;
+    if (tid < RB) {  // per bucket: warp offsets, tile total, global slot run
+#pragma unroll
+      for (int w = 0; w < WARPS; w++) {
+        const uint32_t c = s_wc[w][tid];
+        s_wc[w][tid] = sum;
+        sum += c;
+      }
+      s_base[tid] = sum ? atomicAdd(ctr + tid, sum) : 0u;
+      inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (tid == 31) s_half = inc;
+    }
+    __syncthreads();
+    if (tid < RB) s_start[tid] = inc - sum + (tid >= 32 ? s_half : 0u);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      if (id[j] == 0xffffffffu) continue;
+      const uint32_t b = id[j] >> bshift;
+      const uint32_t p = s_start[b] + s_wc[warp][b] + r[j];
+      s_id[p] = id[j];
+      s_pos[p] = (uint32_t)(base + warp * 32 * KPT + j * 32 + lane);
+    }
+    __syncthreads();
+    const int valid = (int)min((int64_t)TILE, n - base);
+    for (int i = tid; i < valid; i += THREADS) {
+      const uint32_t v = s_id[i];
+      const uint32_t b = v >> bshift;
+      const int64_t g = ((int64_t)b << bshift) + s_base[b] + (uint32_t)i - s_start[b];
+      id_out[g] = v;
+      pos_out[g] = s_pos[i];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_rank_place(const uint32_t *__restrict__ pos, const uint32_t *__restrict__ id, int64_t n,
+                             int32_t *__restrict__ rank) {
+  GRID_STRIDE(i, n) rank[__ldcs(id + i)] = (int32_t)__ldcs(pos + i);
+}
+
 struct Bufs {
   uint32_t *k1, *v1, *k2, *v2;  // ping-pong, n each
   uint32_t *status;             // ceil(n/TILE)*256
@@ -311,6 +415,15 @@ inline int radix_sort(const uint32_t *keys_in, const uint32_t *vals_in, int64_t 
   if (passes < 1) passes = 1;
   if (passes > 4) passes = 4;
   int64_t ntiles = (n + TILE - 1) / TILE;
+  // rank via id buckets when the rank array would not stay in L2 (random
+  // 4-byte writes then cost a DRAM read-modify-write each)
+  static int rb_env = -2;
+  if (rb_env == -2) {
+    const char *e = getenv("LTS_RANK_BUCKET");
+    rb_env = e ? atoi(e) : -1;
+  }
+  const bool bucket_rank = rank_out != nullptr && vals_out != nullptr && n >= (1 << RB_BITS) &&
+                           (rb_env >= 0 ? rb_env == 1 : n * 4 > (int64_t)96 << 20);
   LTS_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * 4 * RADIX, s));
   LTS_CUDA(cudaMemsetAsync(b.ctr, 0, sizeof(uint32_t) * 4, s));
   int hb = grid_blocks(n / 4 + 1, 256, 148 * 4);
@@ -332,7 +445,7 @@ inline int radix_sort(const uint32_t *keys_in, const uint32_t *vals_in, int64_t 
     bool fk = floatkey && p == 0;
     bool hv = cv != nullptr;
     bool wk = ok != nullptr;
-    bool wr = last && rank_out != nullptr;
+    bool wr = last && rank_out != nullptr && !bucket_rank;
 #define LTS_OS(FK, HV, WK, WR) \
   k_onesweep<FK, HV, WK, WR><<<grid, THREADS, 0, s>>>(ck, cv, ok, ov, rank_out, n, sh, offs, b.status, b.ctr + p)
     if (fk) {
@@ -349,6 +462,16 @@ inline int radix_sort(const uint32_t *keys_in, const uint32_t *vals_in, int64_t 
     g_launches++;
     ck = ok;
     cv = ov;
+  }
+  if (bucket_rank) {
+    int lg = 0;
+    while ((int64_t(1) << lg) < n) lg++;
+    const int bshift = lg > RB_BITS ? lg - RB_BITS : 0;
+    LTS_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * RB, s));
+    const int nb = (int)std::min<int64_t>(ntiles, 148 * 4);
+    k_rank_bucket<<<nb, THREADS, 0, s>>>(vals_out, n, bshift, b.k2, b.v2, b.hist);
+    k_rank_place<<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(b.k2, b.v2, n, rank_out);
+    g_launches += 2;
   }
   return 0;
 }
