@@ -455,9 +455,10 @@ __global__ void k_order_keys(const int *rsize, int R, uint32_t *key) {
   GRID_STRIDE(r, R) key[r] = 0x7fffffffu - (uint32_t)rsize[r];
 }
 
+// classified: w.flags / w.ptr already hold this pass's classification of rank
 static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uint8_t *pmark,
                     int max_iter, int *new_rank, int *new_inv, float *g, lts_pass_report_t *rep,
-                    lts_regions_view_t *view) {
+                    lts_regions_view_t *view, bool classified = false) {
   WS &w = c.w;
   const int64_t n = c.n;
   const int ni = (int)n;
@@ -468,7 +469,8 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
   int R = 0, C = 0, S = 0, nshared = 0;
   {
     Phase ph(c, LTS_PH_CLASSIFY);
-    launch_classify(c.g, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
+    if (!classified)
+      launch_classify(c.g, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
     LTS_KCHECK();
   }
   {
@@ -915,8 +917,9 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
   if (n_min > 0) k_set_pmark<<<NB(n_min), 256, 0, s>>>(pres_min, n_min, n, PM_MIN, w.pmark, w.scal + SC_BADPRES);
   else k_set_global<<<1, 32, 0, s>>>(w.invA, n, 0, w.pmark);
   {
+    // extrema of F; the ascent pointers are the first maxima pass's input
     Phase ph(c, LTS_PH_CLASSIFY);
-    launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
+    launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, w.ptr, PTR_ASC, s);
   }
   k_check_pres<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, w.scal + SC_BADPRES);
   k_copy_canon<<<NB(n), 256, 0, s>>>(f, g, n);
@@ -931,7 +934,8 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
   for (it = 1; it <= o.max_iterations; it++) {
     for (int kind = 0; kind < 2; kind++) {
       lts_pass_report_t pr{};
-      LTS_TRY(run_pass(c, kind, cr, ci, w.pmark, o.max_iterations, nr, ni, g, &pr, nullptr));
+      LTS_TRY(run_pass(c, kind, cr, ci, w.pmark, o.max_iterations, nr, ni, g, &pr, nullptr,
+                       it == 1 && kind == 0));
       if (R.n_passes < LTS_MAX_REPORT_PASSES) R.passes[R.n_passes++] = pr;
       std::swap(cr, nr);
       std::swap(ci, ni);

@@ -116,6 +116,9 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t *war
 __device__ long long d_sort_dbg[8];
 __device__ int d_sort_dbg_on;
 
+#ifndef LTS_OS_MATCH
+#define LTS_OS_MATCH 0
+#endif
 #ifndef LTS_OS_MINB
 #define LTS_OS_MINB 4
 #endif
@@ -185,12 +188,16 @@ __global__ void __launch_bounds__(THREADS, LTS_OS_MINB) k_onesweep(
 #pragma unroll
   for (int j = 0; j < KPT; j++) {
     const uint32_t d = (k[j] >> shift) & 255u;
+#if LTS_OS_MATCH
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+#else
     unsigned peers = 0xffffffffu;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
       unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
       peers &= ((d >> b) & 1u) ? bal : ~bal;
     }
+#endif
     const int leader = __ffs(peers) - 1;
     uint32_t cnt = 0;
     if (lane == leader) {

@@ -61,3 +61,36 @@ def test_full_config_bit_exact(cfg):
     assert v.ok
     fz = np.where(f == 0, np.float32(0), f)
     assert np.all(np.isin(gn, fz))
+    # g realises G (non-decreasing along G's order) and never moves a value
+    # past the range of f
+    inv = np.empty_like(Gn)
+    inv[Gn] = np.arange(mesh.n, dtype=np.int32)
+    assert np.all(np.diff(gn[inv]) >= 0)
+    assert gn.min() >= fz.min() and gn.max() <= fz.max()
+
+
+@pytest.mark.parametrize("cfg", [c for c in (1, 3) if str(c) in DATA])
+def test_full_config_determinism_and_idempotence(cfg):
+    """Two runs are bit-identical (parallel schedule independence, SPEC.md:380);
+    simplifying g again with the same constraints and order G changes nothing
+    (idempotence); vertices whose rank did not move keep f."""
+    C = S.CONFIGS[cfg]
+    f = S.make_field(cfg, 0).ravel()
+    mesh = P.build_grid_triangulation(C.dims)
+    fd = torch.from_numpy(f).cuda()
+    F = P.compute_order_field(P.ScalarField(mesh, fd))
+    mn, mx = P.extrema(mesh, F)
+    pm, pn = S.select_preserved(F.rank32.cpu().numpy(), mx.cpu().numpy(), mn.cpu().numpy(),
+                                C.n_keep_max, C.n_keep_min)
+    cs = P.ConstraintSet(preserveMinima=pn, preserveMaxima=pm)
+    g1, G1, _ = P.simplify_field(mesh, fd, cs, order=F)
+    g2, G2, _ = P.simplify_field(mesh, fd, cs, order=F)
+    assert torch.equal(G1.rank32, G2.rank32) and torch.equal(g1.values, g2.values)
+    g3, G3, rep3 = P.simplify_field(mesh, g1.values.clone(), cs, order=G1)
+    assert rep3.ok and rep3.regionCount == 0
+    assert torch.equal(G3.rank32, G1.rank32) and torch.equal(g3.values, g1.values)
+    # locality: a vertex that kept its value kept its place among such vertices
+    fz = torch.where(fd == 0, torch.zeros_like(fd), fd)
+    same = (g1.values == fz)
+    Fr, Gr = F.rank32[same], G1.rank32[same]
+    assert torch.equal(torch.argsort(Fr), torch.argsort(Gr))

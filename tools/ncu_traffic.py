@@ -39,7 +39,7 @@ res = {}
 sort = pick("k_hist<1>", 1) + pick("k_onesweep", 4)  # the first order-field sort
 if len(sort) == 5:
     res["order_sort"] = sum(x[2] for x in sort)
-for key, sub in [("classify", "k_classify_tile<3, 0, 0>"), ("classify_ascent", "k_classify_tile<3, 0, 1>")]:
+for key, sub in [("classify", "k_classify_zreg<0>"), ("classify_ascent", "k_classify_zreg<1>")]:
     sel = pick(sub, 1)
     if sel:
         res[key] = sel[0][2]
