@@ -667,26 +667,78 @@ __device__ __forceinline__ bool claimed_bit(const uint32_t *cbits, int v) {
   return (__ldg(cbits + (v >> 5)) >> (v & 31)) & 1u;
 }
 
-__global__ void k_claimed_flags(const int *__restrict__ inv, int rev, int n,
-                                const uint32_t *__restrict__ cbits, int *flag) {
-  GRID_STRIDE(t, n) {
-    int v = inv[rev ? (n - 1 - t) : t];
-    flag[t] = claimed_bit(cbits, v) ? 1 : 0;
-  }
-}
+// Claimed vertices in rank order as (region, vertex) pairs, in one pass:
+// each thread tests 16 consecutive ranks, a block scan orders the CTA's tile,
+// and a decoupled look-back over the tiles' published counts gives the tile's
+// output offset (replaces flags + a three-kernel scan + compaction).
+// st[0] = tile ticket counter, st[1 + tile] = status (2 flag bits | count).
+constexpr int CC_T = 256, CC_IPT = 16, CC_TILE = CC_T * CC_IPT;
+constexpr int CC_AGG = 1 << 30, CC_PRE = 2 << 30, CC_VAL = (1 << 30) - 1;
 
-__global__ void k_claimed_compact(const int *__restrict__ inv, int rev, int n,
-                                  const uint32_t *__restrict__ cbits, const int *__restrict__ reg_of,
-                                  const int *__restrict__ pos, uint32_t *ckey, uint32_t *cval) {
-  GRID_STRIDE(t, n) {
-    int v = inv[rev ? (n - 1 - t) : t];
-    if (claimed_bit(cbits, v)) {
-      int rid = reg_of[v];
-      int p = pos[t];
-      ckey[p] = (uint32_t)rid;
-      cval[p] = (uint32_t)v;
-    }
+__global__ void __launch_bounds__(CC_T) k_claimed_compact_lb(const int *__restrict__ inv, int rev, int n,
+                                                           const uint32_t *__restrict__ cbits,
+                                                           const int *__restrict__ reg_of, uint32_t *ckey,
+                                                           uint32_t *cval, int *st, int *total) {
+  __shared__ int s_tile, s_base, s_wsum[CC_T / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(st, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t t0 = (int64_t)tile * CC_TILE + (int64_t)tid * CC_IPT;
+  int v[CC_IPT];
+  unsigned fl = 0;
+#pragma unroll
+  for (int j = 0; j < CC_IPT; j++) {
+    const int64_t t = t0 + j;
+    v[j] = t < n ? __ldg(inv + (rev ? (n - 1 - t) : t)) : 0;
+    if (t < n && claimed_bit(cbits, v[j])) fl |= 1u << j;
   }
+  const int c = __popc(fl);
+  int inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_wsum[warp] = inc;
+  __syncthreads();
+  int pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < CC_T / 32; w++) {
+    const int x = s_wsum[w];
+    pre += w < warp ? x : 0;
+    tot += x;
+  }
+  if (tid == 0) {
+    volatile int *S = st + 1;
+    int base = 0;
+    if (tile == 0) {
+      S[0] = CC_PRE | tot;
+    } else {
+      S[tile] = CC_AGG | tot;
+      int acc = 0;
+      for (int64_t p = tile - 1; p >= 0;) {
+        const int sv = S[p];
+        if ((sv & ~CC_VAL) == 0) continue;  // predecessor not published yet
+        acc += sv & CC_VAL;
+        if ((sv & ~CC_VAL) == CC_PRE) break;
+        p--;
+      }
+      base = acc;
+      S[tile] = CC_PRE | (acc + tot);
+    }
+    s_base = base;
+    if ((int64_t)(tile + 1) * CC_TILE >= n) *total = base + tot;
+  }
+  __syncthreads();
+  int p = s_base + pre + inc - c;
+#pragma unroll
+  for (int j = 0; j < CC_IPT; j++)
+    if (fl >> j & 1u) {
+      ckey[p] = (uint32_t)reg_of[v[j]];
+      cval[p] = (uint32_t)v[j];
+      p++;
+    }
 }
 
 // region sizes (+1 for the saddle) -> scan input

@@ -573,15 +573,19 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     k_region_slots<<<NB(R), 256, 0, s>>>(w.rsize, R, w.rtmp);
     g_launches++;
     LTS_TRY(scan_int(w.rtmp, w.rptr, R, w.bsum, w.scal + SC_S, false, s));
-    k_claimed_flags<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.cbits, w.flagscan);
-    g_launches++;
-    LTS_TRY(scan_int(w.flagscan, w.flagscan, n, w.bsum, w.scal + SC_C, false, s));
+    {
+      const int cc_tiles = (int)((n + CC_TILE - 1) / CC_TILE);
+      LTS_CUDA(cudaMemsetAsync(w.flagscan, 0, sizeof(int) * (cc_tiles + 1), s));
+      LTS_CUDA(cudaMemsetAsync(w.scal + SC_C, 0, sizeof(int), s));
+      if (cc_tiles > 0)
+        k_claimed_compact_lb<<<cc_tiles, CC_T, 0, s>>>(inv, rev, ni, w.cbits, w.reg_of, w.ckey, w.cval,
+                                                     w.flagscan, w.scal + SC_C);
+      g_launches++;
+    }
     LTS_TRY(readback(c, SC_S, 2));
     S = c.h_scal[SC_S];
     C = c.h_scal[SC_C];
     LTS_CUDA(cudaMemcpyAsync(w.rptr + R, w.scal + SC_S, sizeof(int), cudaMemcpyDeviceToDevice, s));
-    k_claimed_compact<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.cbits, w.reg_of, w.flagscan, w.ckey, w.cval);
-    g_launches++;
     LTS_TRY(radix_sort(w.ckey, w.cval, C, bits_for(R - 1), false, w.skey, w.sval, nullptr, w.sb, s));
     k_place<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, w.loc_of);
     k_place_saddles<<<NB(R), 256, 0, s>>>(inv, rev, ni, w.rsad, R, w.rptr, w.verts);
