@@ -652,3 +652,128 @@ void orc_realize_sweep_f32(float *gv, const int32_t *inverse, int64_t n) {
     prev = v;
   }
 }
+
+/* ------------------------------------------------------------------------- */
+/* truncated extremum-saddle pairing: _kernels.py:309-421 (pairs_sweep)        */
+/* Descending propagations from every seed maximum; a component stops once    */
+/* its drop from its highest seed reaches eps (persistent) or it meets spent  */
+/* territory; the younger components meeting at a junction die there and are  */
+/* paired with it when their drop is below eps (Elder rule).                  */
+/* pair_saddle[i] = junction vertex of seeds[i], or -1 (survivor).            */
+/* ------------------------------------------------------------------------- */
+
+int orc_pairs_sweep(const int32_t *rank, const double *values, int ndim, const int64_t *dims,
+                    const int32_t *seeds, int64_t nseeds, double eps, int32_t *pair_saddle) {
+  grid_t g;
+  if (grid_init(&g, ndim, dims)) return -1;
+  int64_t n = g.n;
+  int8_t *state = (int8_t *)malloc((size_t)n);
+  int32_t *owner = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  int32_t *seedslot = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  int32_t *parent = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nseeds + 1));
+  int32_t *topslot = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nseeds + 1));
+  uint8_t *stopped = (uint8_t *)calloc((size_t)(nseeds + 1), 1);
+  heap_t h;
+  h.key = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  h.val = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  h.size = 0;
+  for (int64_t v = 0; v < n; v++) {
+    state[v] = ORC_UNTOUCHED;
+    owner[v] = -1;
+    seedslot[v] = -1;
+  }
+  for (int64_t i = 0; i < nseeds; i++) {
+    parent[i] = (int32_t)i;
+    topslot[i] = (int32_t)i;
+    pair_saddle[i] = -1;
+    seedslot[seeds[i]] = (int32_t)i;
+  }
+  for (int64_t i = 0; i < nseeds; i++) {
+    hpush(&h, rank[seeds[i]], seeds[i]);
+    state[seeds[i]] = ORC_PENDING;
+  }
+  int err = 0;
+  int64_t roots[14];
+  while (h.size > 0) {
+    int64_t rv;
+    int64_t v = hpop(&h, &rv);
+    if (state[v] >= ORC_CLAIMED) continue;
+    if (seedslot[v] >= 0) { /* a seed claims itself and opens its link (:343-351) */
+      owner[v] = seedslot[v];
+      state[v] = ORC_CLAIMED;
+      for (int k = 0; k < g.K; k++) {
+        int64_t u = nbr(&g, v, k);
+        if (u >= 0 && state[u] == ORC_UNTOUCHED) {
+          state[u] = ORC_PENDING;
+          hpush(&h, rank[u], u);
+        }
+      }
+      continue;
+    }
+    int beyond = 0, nroots = 0; /* upper link (:353-372) */
+    for (int k = 0; k < g.K; k++) {
+      int64_t u = nbr(&g, v, k);
+      if (u < 0 || rank[u] <= rv) continue;
+      if (state[u] == ORC_CLAIMED) {
+        int64_t r = uf_find64(parent, owner[u]);
+        int seen = 0;
+        for (int j = 0; j < nroots; j++)
+          if (roots[j] == r) seen = 1;
+        if (!seen) roots[nroots++] = r;
+        if (stopped[r]) beyond = 1;
+      } else {
+        beyond = 1;
+      }
+    }
+    if (nroots == 0) { /* :374-377 */
+      err = 1;
+      state[v] = ORC_FRINGE;
+      continue;
+    }
+    int64_t elder = -1; /* the root with the highest seed (:379-384) */
+    if (!beyond) {
+      elder = roots[0];
+      for (int j = 1; j < nroots; j++)
+        if (rank[seeds[topslot[roots[j]]]] > rank[seeds[topslot[elder]]]) elder = roots[j];
+    }
+    for (int j = 0; j < nroots; j++) { /* the others stop here (:386-393) */
+      int64_t r = roots[j];
+      if (r == elder || stopped[r]) continue;
+      stopped[r] = 1;
+      if (values[seeds[topslot[r]]] - values[v] < eps) pair_saddle[topslot[r]] = (int32_t)v;
+    }
+    int64_t root = roots[0]; /* merge (:395-402) */
+    for (int j = 1; j < nroots; j++) {
+      int64_t ra = uf_find64(parent, root), rb = uf_find64(parent, roots[j]);
+      if (ra != rb) {
+        parent[rb] = (int32_t)ra;
+        if (rank[seeds[topslot[rb]]] > rank[seeds[topslot[ra]]]) topslot[ra] = topslot[rb];
+        root = ra;
+      }
+    }
+    int64_t r = uf_find64(parent, root);
+    owner[v] = (int32_t)r;
+    state[v] = ORC_CLAIMED;
+    if (beyond || values[seeds[topslot[r]]] - values[v] >= eps) { /* :406-408 */
+      stopped[r] = 1;
+      continue;
+    }
+    stopped[r] = 0;
+    for (int k = 0; k < g.K; k++) {
+      int64_t u = nbr(&g, v, k);
+      if (u >= 0 && state[u] == ORC_UNTOUCHED) {
+        state[u] = ORC_PENDING;
+        hpush(&h, rank[u], u);
+      }
+    }
+  }
+  free(state);
+  free(owner);
+  free(seedslot);
+  free(parent);
+  free(topslot);
+  free(stopped);
+  free(h.key);
+  free(h.val);
+  return err;
+}

@@ -58,6 +58,7 @@ def lib():
         L.orc_integrate.argtypes = [P, i64, P, i64, P, P, P, P]
         L.orc_integrate.restype = i64
         L.orc_realize_sweep_f32.argtypes = [P, P, i64]
+        L.orc_pairs_sweep.argtypes = [P, P, i32, P, P, i64, ctypes.c_double, P]
         _lib = L
     return _lib
 
@@ -159,6 +160,28 @@ def integrate(rank, region_ptr, region_verts, local, topseed_rank):
     if coll:
         raise OracleError(f"integration key collision ({coll})")
     return out
+
+
+def pairs(dims, rank: np.ndarray, values: np.ndarray, kind: str = "max", eps: float = float("inf")):
+    """Truncated extremum-saddle pairs (reference pairs_sweep, _kernels.py:309-421)
+    from every maximum (kind "max") or every minimum (kind "min": the same sweep
+    on the reversed order n-1-rank and negated values, SPEC persistence).
+    Returns (extrema ids ascending, pair saddle per extremum or -1 = survivor, err)."""
+    rank = np.ascontiguousarray(rank, np.int32)
+    values = np.ascontiguousarray(values, np.float64)
+    n = rank.size
+    mn, mx = extrema(dims, rank)
+    if kind == "max":
+        seeds, r, v = mx, rank, values
+    else:
+        seeds, r, v = mn, np.ascontiguousarray(n - 1 - rank, np.int32), np.ascontiguousarray(-values)
+    seeds = np.ascontiguousarray(np.sort(seeds), np.int32)
+    out = np.full(seeds.size, -1, np.int32)
+    err = lib().orc_pairs_sweep(_p(r), _p(v), len(dims), _p(_dims(dims)), _p(seeds), seeds.size,
+                                float(eps), _p(out))
+    if err < 0:
+        raise OracleError("bad grid")
+    return seeds.astype(np.int64), out.astype(np.int64), int(err)
 
 
 def realize_sweep_f32(g: np.ndarray, inverse: np.ndarray) -> None:

@@ -1,0 +1,84 @@
+"""Persistence-driven mode (reference pairs_sweep, _kernels.py:309-421; SPEC
+persistence module).  The C oracle's restatement is pinned to fixtures made by
+running the reference's own numba pairs_sweep (tests/golden/make_pairs_golden.py);
+the GPU pairing (maxima graph -> maximum spanning forest -> Elder-rule sweep)
+must reproduce the oracle exactly, extremum by extremum, for every epsilon."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from oracle import lts_oracle as O
+
+GOLD = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "pairs", "*.npz")))
+IDS = [os.path.basename(p)[:-4] for p in GOLD]
+
+
+def _load(p):
+    z = np.load(p)
+    return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("path", GOLD, ids=IDS)
+def test_oracle_pairs_match_reference(path):
+    z = _load(path)
+    dims = tuple(int(d) for d in z["dims"])
+    rank, _ = O.order_field(z["f"])
+    vals = z["f"].astype(np.float64)
+    for kind in ("max", "min"):
+        for i, e in enumerate(z["eps"]):
+            seeds, sad, err = O.pairs(dims, rank, vals, kind, e)
+            assert err == 0
+            np.testing.assert_array_equal(seeds, z[f"{kind}_seeds"])
+            np.testing.assert_array_equal(sad, z[f"{kind}_saddle_{i}"])
+
+
+def _case(path):
+    z = _load(path)
+    return tuple(int(d) for d in z["dims"]), z["f"], z["eps"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", GOLD, ids=IDS)
+def test_gpu_pairs_golden(path):
+    import torch
+
+    import paper_2009_00083_b200 as P
+    dims, f, eps = _case(path)
+    z = _load(path)
+    mesh = P.build_grid_triangulation(dims)
+    fd = torch.from_numpy(f).cuda()
+    for kind in ("max", "min"):
+        for i, e in enumerate(eps):
+            pr = P.compute_extremum_saddle_pairs(mesh, fd, polarity=kind, epsilon=float(e))
+            ext = pr.extrema.cpu().numpy()
+            sad = pr.saddles.cpu().numpy()
+            np.testing.assert_array_equal(ext, z[f"{kind}_seeds"])
+            np.testing.assert_array_equal(sad, z[f"{kind}_saddle_{i}"])
+
+
+GPU_CASES = {
+    "rand2d_300x200": lambda: np.random.default_rng(21).random((200, 300)).astype(np.float32),
+    "quant3d_40": lambda: (np.round(np.random.default_rng(22).random((40, 40, 40)) * 30) / 30).astype(np.float32),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(GPU_CASES))
+def test_gpu_pairs_vs_oracle(name):
+    import torch
+
+    import paper_2009_00083_b200 as P
+    f = GPU_CASES[name]()
+    dims = f.shape[::-1]
+    rank, _ = O.order_field(f.ravel())
+    mesh = P.build_grid_triangulation(dims)
+    fd = torch.from_numpy(f.ravel()).cuda()
+    fr = float(f.max() - f.min())
+    for kind in ("max", "min"):
+        for e in (float("inf"), 0.05 * fr, 0.25 * fr):
+            seeds, sad, err = O.pairs(dims, rank, f.ravel().astype(np.float64), kind, e)
+            pr = P.compute_extremum_saddle_pairs(mesh, fd, polarity=kind, epsilon=e)
+            np.testing.assert_array_equal(pr.extrema.cpu().numpy(), seeds)
+            np.testing.assert_array_equal(pr.saddles.cpu().numpy(), sad)
