@@ -151,6 +151,18 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
                  float *g, int32_t *G, lts_report_t *rep, const lts_options_t *opt, void *ws,
                  size_t ws_bytes, void *stream);
 
+/* Extremum-saddle pairs of the persistence-driven mode (reference
+ * pairs_sweep, _kernels.py:309-421): kind 0 pairs every
+ * maximum, kind 1 every minimum (reversed order, negated values).  Outputs,
+ * each of n entries (the first *count_out used): extrema_out = extremum vertex
+ * ids ascending, saddle_out = the junction vertex each one dies at when its
+ * persistence |f(extremum) - f(saddle)| (float64) is below epsilon, else -1
+ * (survivor, including the global extremum).  order may be NULL (computed
+ * from f).  Synchronous on the stream (returns after the pairs are written). */
+int lts_extremum_pairs(const float *f, const int32_t *order, int ndim, const int64_t *dims, int kind,
+                       double epsilon, int32_t *extrema_out, int32_t *saddle_out, int64_t *count_out, void *ws,
+                       size_t ws_bytes, void *stream);
+
 /* Roofline micro-benchmarks (diagnostics): L2 flushed before each rep, CUDA
  * events around the kernel(s) only.  out_ms (host, 4): [0] order-field sort,
  * [1] classification (flags), [2] classification + ascent pointer, [3] 0. */

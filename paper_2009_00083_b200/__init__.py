@@ -14,6 +14,8 @@ from .critical import (CriticalSet, Criticality, Kind, classify_all, classify_ve
                        extract_critical_points, extrema)
 from .engine import (ConstraintSet, PassRegions, SimplifyOptions, SimplifyReport, discover_regions,
                      remove_extrema, remove_pass, simplify_field, simplify_raw, verify_constraints)
+from .persistence import (PersistencePairs, compute_extremum_saddle_pairs, persistence_curve,
+                          persistence_simplify)
 
 __all__ = [
     "ConstraintNotExtremum", "FieldError", "LocalizeError", "LTSNativeError", "MeshError",
@@ -22,5 +24,6 @@ __all__ = [
     "order_from_ranks", "CriticalSet", "Criticality", "Kind", "classify_all", "classify_vertex",
     "extract_critical_points", "extrema", "ConstraintSet", "PassRegions", "SimplifyOptions",
     "SimplifyReport", "discover_regions", "remove_extrema", "remove_pass", "simplify_field",
-    "simplify_raw", "verify_constraints",
+    "simplify_raw", "verify_constraints", "PersistencePairs", "compute_extremum_saddle_pairs",
+    "persistence_curve", "persistence_simplify",
 ]

@@ -62,7 +62,8 @@ class lts_regions_view_t(ctypes.Structure):
 
 
 EXPORTS = ["lts_version", "lts_last_error", "lts_workspace_size", "lts_order_field", "lts_classify",
-           "lts_remove_pass", "lts_simplify", "lts_kernel_launches", "lts_debug_big_stats", "lts_bench_kernels"]
+           "lts_remove_pass", "lts_simplify", "lts_kernel_launches", "lts_debug_big_stats", "lts_bench_kernels",
+           "lts_extremum_pairs"]
 
 _lib = None
 
@@ -93,6 +94,8 @@ def load():
                                ctypes.POINTER(lts_options_t), P, ctypes.c_size_t, P]
     L.lts_debug_big_stats.argtypes = [I, P, I]
     L.lts_bench_kernels.argtypes = [P, I, P, I, P, P, ctypes.c_size_t, P]
+    L.lts_extremum_pairs.argtypes = [P, P, I, P, I, ctypes.c_double, P, P, ctypes.POINTER(I64), P,
+                                     ctypes.c_size_t, P]
     for name in EXPORTS:
         getattr(L, name)
     _lib = L

@@ -26,6 +26,7 @@
 #include "localize.cuh"
 #include "localize_big.cuh"
 #include "integrate.cuh"
+#include "persistence.cuh"
 
 namespace lts {
 int64_t g_launches = 0;
@@ -758,6 +759,142 @@ int64_t lts_kernel_launches(void) { return g_launches; }
 // directly around it on `stream`.  out_ms[0] order-field sort (histogram +
 // 4 onesweep passes + rank scatter), [1] classification (flags), [2]
 // classification + ascent pointer, [3] mean onesweep pass.  Averages over reps.
+// ---------------------------------------------------------------------------
+// persistence-driven mode: extremum-saddle pairs (persistence.cuh)
+// ---------------------------------------------------------------------------
+static int order_field_impl(Ctx &c, const float *f, int32_t *rank, int32_t *inverse);
+
+static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, int kind, double eps,
+                      int32_t *ext_out, int32_t *sad_out, int64_t *count_out) {
+  WS &w = c.w;
+  const int64_t n = c.n;
+  const int ni = (int)n;
+  const int rev = kind;
+  cudaStream_t s = c.s;
+  // every extremum of the polarity is a seed: no preserve marks
+  LTS_CUDA(cudaMemsetAsync(w.pmark, 0, (size_t)n, s));
+  LTS_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(int) * SC_N, s));
+  launch_classify(c.g, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
+  k_mark_maxima<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, kind, n, w.vcls, w.cst, w.mlist, w.scal + SC_COUNTS,
+                                       w.comp, w.par, w.acc, w.rpar, w.bestP);
+  for (int j = 0; j < 3; j++) k_jump<<<NB(n), 256, 0, s>>>(w.ptr, n);
+  k_compress<<<NB(n), 256, 0, s>>>(w.ptr, n);
+  k_roots<<<NB(n), 256, 0, s>>>(w.ptr, n, w.M);
+  g_launches += 7;
+  LTS_KCHECK();
+  LTS_TRY(readback(c, SC_COUNTS, 3));
+  const int nm = c.h_scal[SC_COUNTS];
+  *count_out = nm;
+  if (nm == 0) return 0;
+  // extrema in ascending vertex order = node order
+  LTS_TRY(radix_sort((const uint32_t *)w.mlist, nullptr, nm, bits_for(ni - 1), false, w.ckey, w.cval, nullptr,
+                     w.sb, s));
+  int *idx = w.delta, *nrank = w.rt, *comp = w.comp, *par = w.par, *pair = w.acc, *rt = w.wc;
+  k_pn_index<<<NB(nm), 256, 0, s>>>(w.ckey, nm, idx, rank, rev, ni, nrank, comp, pair);
+  g_launches++;
+  // maxima-graph edges (hash-deduplicated per manifold pair; list fallback)
+  int hbits = 12;
+  while (hbits < 30 && (1ll << hbits) < 64ll * nm) hbits++;
+  while (hbits > 10 && 18ll << hbits > 12 * w.emax) hbits--;
+  EdgeHash H{(unsigned long long *)w.ebuf, (int *)(w.ebuf + (8ll << hbits)), hbits, w.scal + SC_ECOUNT,
+             w.scal + SC_ACTIVE};
+  int *ea = w.ea, *eb = w.eb, *ew = w.ew;
+  for (int mode = 0; mode < 2; mode++) {
+    if (mode == 0) {
+      ea = (int *)(w.ebuf + (12ll << hbits));
+      eb = ea + (1ll << (hbits - 1));
+      ew = eb + (1ll << (hbits - 1));
+      LTS_CUDA(cudaMemsetAsync(w.ebuf, 0xff, 12ull << hbits, s));
+    } else {
+      H.bits = 0;
+      ea = w.ea; eb = w.eb; ew = w.ew;
+      LTS_CUDA(cudaMemsetAsync(w.scal + SC_ECOUNT, 0, sizeof(int) * 2, s));
+    }
+    dim3 eg((c.g.nx + ET_TX - 1) / ET_TX, (c.g.ny + ET_TY - 1) / ET_TY,
+            c.g.ndim == 2 ? 1 : (c.g.nz + ET_ZC - 1) / ET_ZC);
+    dim3 eb3(ET_TX, ET_TY);
+    if (c.g.ndim == 2)
+      k_edges_tile<2><<<eg, eb3, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
+    else
+      k_edges_tile<3><<<eg, eb3, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
+    g_launches++;
+    if (mode == 0) {
+      k_hash_compact<<<NB(1ll << hbits), 256, 0, s>>>(H, ea, eb, ew, w.scal + SC_TMP);
+      g_launches++;
+    }
+    LTS_KCHECK();
+    LTS_TRY(readback(c, SC_ECOUNT, 2));
+    if (mode == 0 && c.h_scal[SC_ACTIVE] == 0) break;
+  }
+  const int ne = c.h_scal[SC_ECOUNT];
+  int *ia = w.nrowkey, *ib = w.nrowkey + w.emax, *mst = w.nrow;
+  if (ne > 0) {
+    k_pn_edges<<<NB(ne), 256, 0, s>>>(ea, eb, ne, idx, ia, ib, mst);
+    g_launches++;
+  }
+  // maximum spanning forest (Boruvka)
+  for (int round = 0; round < 64 && ne > 0; round++) {
+    LTS_CUDA(cudaMemsetAsync(w.scal + SC_ACTIVE, 0, sizeof(int), s));
+    k_pn_reset<<<NB(nm), 256, 0, s>>>(nm, w.best);
+    k_pn_best<<<NB(ne), 256, 0, s>>>(ia, ib, ew, ne, comp, w.best);
+    k_pn_hook<<<NB(nm), 256, 0, s>>>(nm, comp, w.best, ia, ib, par, mst, w.scal + SC_ACTIVE);
+    k_pn_cycle<<<NB(nm), 256, 0, s>>>(nm, comp, par);
+    k_pn_roots<<<NB(nm), 256, 0, s>>>(nm, comp, par, rt);
+    k_pn_relabel<<<NB(nm), 256, 0, s>>>(nm, comp, rt);
+    g_launches += 6;
+    LTS_KCHECK();
+    LTS_TRY(readback(c, SC_ACTIVE, 1));
+    if (c.h_scal[SC_ACTIVE] == 0) break;
+  }
+  // forest edges by decreasing weight, then the Elder-rule sweep
+  int cnt = 0;
+  if (ne > 0) {
+    LTS_CUDA(cudaMemsetAsync(w.scal + SC_TMP, 0, sizeof(int), s));
+    k_pn_mst_keys<<<NB(ne), 256, 0, s>>>(mst, ew, ne, ni, (uint32_t *)w.rtmp, (uint32_t *)w.okey,
+                                         w.scal + SC_TMP);
+    g_launches++;
+    LTS_TRY(readback(c, SC_TMP, 1));
+    cnt = c.h_scal[SC_TMP];
+  }
+  if (cnt > 0) {
+    LTS_TRY(radix_sort((const uint32_t *)w.rtmp, (const uint32_t *)w.okey, cnt, bits_for(ni - 1), false, w.okey2,
+                       w.oval, nullptr, w.sb, s));
+    const size_t shm = sizeof(int) * 2 * (size_t)nm;
+    const int use_smem = shm <= 200 * 1024;
+    if (use_smem) LTS_CUDA(cudaFuncSetAttribute(k_pn_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    k_pn_sweep<<<1, 32, use_smem ? shm : 0, s>>>(w.oval, cnt, ia, ib, ew, nrank, nm, par, comp, use_smem,
+                                                 (int *)w.skey, (int *)w.sval);
+    k_pn_pairs<<<NB(cnt), 256, 0, s>>>((const int *)w.skey, (const int *)w.sval, cnt, inv, rev, ni, f, eps, idx,
+                                       pair);
+    g_launches += 2;
+  }
+  k_pn_out<<<NB(nm), 256, 0, s>>>(w.ckey, pair, nm, ext_out, sad_out);
+  g_launches++;
+  LTS_KCHECK();
+  return 0;
+}
+
+int lts_extremum_pairs(const float *f, const int32_t *order, int ndim, const int64_t *dims, int kind, double epsilon,
+                       int32_t *extrema_out, int32_t *saddle_out, int64_t *count_out, void *ws, size_t ws_bytes,
+                       void *stream) {
+  Ctx c;
+  LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
+  if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
+  if (kind != 0 && kind != 1) return lts_set_error(LTS_E_INVALID, "kind must be 0 (maxima) or 1 (minima)");
+  if (!(epsilon >= 0)) return lts_set_error(LTS_E_INVALID, "epsilon must be >= 0");
+  WS &w = c.w;
+  if (order) {
+    LTS_CUDA(cudaMemcpyAsync(w.rankA, order, sizeof(int) * c.n, cudaMemcpyDeviceToDevice, c.s));
+    k_scatter_inverse<<<NB(c.n), 256, 0, c.s>>>(w.rankA, w.invA, c.n);
+    g_launches++;
+  } else {
+    LTS_TRY(order_field_impl(c, f, w.rankA, w.invA));
+  }
+  LTS_TRY(pairs_impl(c, f, w.rankA, w.invA, kind, epsilon, extrema_out, saddle_out, count_out));
+  LTS_CUDA(cudaStreamSynchronize(c.s));
+  return 0;
+}
+
 int lts_bench_kernels(const float *f, int ndim, const int64_t *dims, int reps, double *out_ms, void *ws,
                       size_t ws_bytes, void *stream) {
   Ctx c;

@@ -82,3 +82,51 @@ def test_gpu_pairs_vs_oracle(name):
             pr = P.compute_extremum_saddle_pairs(mesh, fd, polarity=kind, epsilon=e)
             np.testing.assert_array_equal(pr.extrema.cpu().numpy(), seeds)
             np.testing.assert_array_equal(pr.saddles.cpu().numpy(), sad)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("frac", [0.0, 0.05, 0.3, 2.0])
+def test_gpu_persistence_simplify(frac):
+    """discard sets = non-surviving extrema of both
+    polarities; the result equals the oracle LTS pass with the oracle's
+    survivors preserved, ||f - g||_inf <= epsilon, and epsilon beyond the value
+    range leaves exactly one minimum and one maximum."""
+    import torch
+
+    import paper_2009_00083_b200 as P
+    f = (np.round(np.random.default_rng(31).random((48, 56)) * 64) / 64).astype(np.float32)
+    dims = f.shape[::-1]
+    fv = f.ravel()
+    eps = frac * float(fv.max() - fv.min())
+    rank, _ = O.order_field(fv)
+    smax, pmax, _ = O.pairs(dims, rank, fv.astype(np.float64), "max", eps)
+    smin, pmin, _ = O.pairs(dims, rank, fv.astype(np.float64), "min", eps)
+    keep_max, keep_min = smax[pmax < 0], smin[pmin < 0]
+    ref = O.simplify(dims, fv, keep_max, keep_min)
+    mesh = P.build_grid_triangulation(dims)
+    g, G, (qmax, qmin), rep = P.persistence_simplify(mesh, torch.from_numpy(fv).cuda(), eps)
+    np.testing.assert_array_equal(qmax.survivors.cpu().numpy(), keep_max)
+    np.testing.assert_array_equal(qmin.survivors.cpu().numpy(), keep_min)
+    assert rep.ok == ref.ok
+    np.testing.assert_array_equal(G.rank32.cpu().numpy(), ref.G_rank)
+    assert g.values.cpu().numpy().tobytes() == ref.g.tobytes()
+    assert float(np.abs(g.values.cpu().numpy().astype(np.float64) - fv).max()) <= eps
+    if frac == 0.0:
+        assert np.array_equal(g.values.cpu().numpy(), fv)
+    if frac > 1.0:
+        mn, mx = P.extrema(mesh, G)
+        assert mn.numel() == 1 and mx.numel() == 1
+
+
+def test_persistence_curve_monotone():
+    import types
+    import torch
+
+    from paper_2009_00083_b200.persistence import PersistencePairs, persistence_curve
+    p = PersistencePairs("max", float("inf"), torch.tensor([1, 2, 3]), torch.tensor([5, 6, -1]),
+                         torch.tensor([2.0, 0.5, float("inf")], dtype=torch.float64))
+    thr, cnt = persistence_curve(p, value_range=9.0)
+    assert thr.tolist() == [0.5, 2.0, 9.0] and cnt.tolist() == [3, 2, 1]
+    assert np.all(np.diff(cnt) <= 0)
+    thr, cnt = persistence_curve([], None)
+    assert thr.size == 0 and cnt.size == 0
