@@ -6,14 +6,19 @@
     python -m paper_2009_00083_b200.cli verify --original F --simplified G --order O.npy --preserve LIST
     python -m paper_2009_00083_b200.cli bench --input F (--preserve LIST | --keep-max K --keep-min K)
             [--repeat N]
+    python -m paper_2009_00083_b200.cli simplify --input F --epsilon E[%] --output G
+    python -m paper_2009_00083_b200.cli diagram --input F [--epsilon E[%]] --output D.json
+            [--polarity max|min|both]
+    python -m paper_2009_00083_b200.cli curve --input F --output C.json
     python -m paper_2009_00083_b200.cli synth --config C [--seed S] --output F
 
 Fields are SFG text or SFGB binary (``paper_2009_00083_b200.io``); the
 preserve list holds vertex ids of maxima and minima of the input order, one per
 line, split by classification.  ``--keep-max/--keep-min`` select the K highest
 maxima / K lowest minima of the input order instead (the BASELINE
-configs' selection rule).  ``--epsilon`` (the persistence-driven mode, SPEC
-persistence module) is not part of this build and exits with usage status 2.
+configs' selection rule).  ``--epsilon E`` (field units, or ``E%`` of the
+value range) selects the persistence-driven mode instead: every
+extremum less persistent than E is removed (SPEC persistence module).
 ``--threads`` is accepted and ignored (the work runs on the GPU).
 Exit codes: 0 success, 1 verification failure, 2 usage.
 """
@@ -58,22 +63,41 @@ def _constraints(args, mesh, fd):
     return F, ConstraintSet(preserveMinima=pmin, preserveMaxima=pmax)
 
 
-def _need_selection(ap, args):
-    if args.epsilon is not None:
-        ap.error("--epsilon (persistence-driven mode) is not part of this build; use --preserve or --keep-max/--keep-min")
-    if not args.preserve and (args.keep_max is None or args.keep_min is None):
-        ap.error("give --preserve LIST or both --keep-max and --keep-min")
-    if args.preserve and (args.keep_max is not None or args.keep_min is not None):
-        ap.error("--preserve conflicts with --keep-max/--keep-min")
+def _need_selection(ap, args, epsilon_ok=False):
+    chosen = [args.epsilon is not None, bool(args.preserve), args.keep_max is not None or args.keep_min is not None]
+    if sum(chosen) != 1:
+        ap.error("give exactly one of --epsilon, --preserve LIST, or --keep-max K --keep-min K")
+    if args.epsilon is not None and not epsilon_ok:
+        ap.error("--epsilon is not accepted by this subcommand")
+    if chosen[2] and (args.keep_max is None or args.keep_min is None):
+        ap.error("--keep-max and --keep-min go together")
+
+
+def _epsilon(text, fd) -> float:
+    """E (field units) or E% of the value range."""
+    t = str(text).strip()
+    try:
+        if t.endswith("%"):
+            return float(t[:-1]) / 100.0 * float(fd.max() - fd.min())
+        return float(t)
+    except ValueError:
+        raise FieldError(f"--epsilon {t!r} is not a number or a percentage") from None
 
 
 def cmd_simplify(ap, args) -> int:
-    _need_selection(ap, args)
-    from . import SimplifyOptions, simplify_field
+    _need_selection(ap, args, epsilon_ok=True)
+    from . import ConstraintSet, SimplifyOptions, persistence_simplify, simplify_field
     dims, mesh, fd = _load(args.input)
-    F, cs = _constraints(args, mesh, fd)
     opt = SimplifyOptions(restoreInteriorExtrema=not args.no_restore, maxIterations=args.max_iterations)
-    g, G, rep = simplify_field(mesh, fd, cs, opt, order=F)
+    if args.epsilon is not None:
+        eps = _epsilon(args.epsilon, fd)
+        if eps < 0:
+            ap.error("--epsilon must be >= 0")
+        g, G, (pmax, pmin), rep = persistence_simplify(mesh, fd, eps, opt)
+        cs = ConstraintSet(preserveMinima=pmin.survivors.cpu().numpy(), preserveMaxima=pmax.survivors.cpu().numpy())
+    else:
+        F, cs = _constraints(args, mesh, fd)
+        g, G, rep = simplify_field(mesh, fd, cs, opt, order=F)
     sio.write_field(args.output, dims, g.values.cpu().numpy())
     if args.order_out:
         np.save(args.order_out, G.rank32.cpu().numpy().astype(np.int64))
@@ -149,6 +173,52 @@ def cmd_bench(ap, args) -> int:
     return 0
 
 
+def _pairs(mesh, fd, polarity, eps):
+    from . import ScalarField, compute_extremum_saddle_pairs, compute_order_field
+    f = ScalarField(mesh, fd)
+    F = compute_order_field(f)
+    kinds = ["max", "min"] if polarity == "both" else [polarity]
+    return [compute_extremum_saddle_pairs(mesh, f, F, k, eps) for k in kinds]
+
+
+def cmd_diagram(ap, args) -> int:
+    """Diagram JSON: pairs below epsilon plus the survivors
+    (saddleVertex null); a survivor's persistence is the value range for the
+    global extremum (the global pair convention) and null for the
+    others when epsilon is finite."""
+    dims, mesh, fd = _load(args.input)
+    eps = _epsilon(args.epsilon, fd) if args.epsilon is not None else float("inf")
+    f = fd.cpu().numpy().astype(np.float64)
+    vr = float(f.max() - f.min())
+    out = []
+    for pp in _pairs(mesh, fd, args.polarity, eps):
+        pol = "MaxSaddle" if pp.polarity == "max" else "MinSaddle"
+        ext = pp.extrema.cpu().numpy()
+        sad = pp.saddles.cpu().numpy()
+        glob_ext = int(ext[np.argmax(f[ext])]) if pp.polarity == "max" else int(ext[np.argmin(f[ext])])
+        for e, sv in zip(ext.tolist(), sad.tolist()):
+            if sv >= 0:
+                out.append({"extremumVertex": e, "saddleVertex": sv, "birth": f[e], "death": f[sv],
+                            "persistence": abs(f[e] - f[sv]), "polarity": pol})
+            else:
+                out.append({"extremumVertex": e, "saddleVertex": None, "birth": f[e], "death": None,
+                            "persistence": vr if e == glob_ext else None, "polarity": pol})
+    with open(args.output, "w") as fh:
+        json.dump(out, fh)
+    return 0
+
+
+def cmd_curve(ap, args) -> int:
+    """Curve JSON: both polarities, full diagram."""
+    from . import persistence_curve
+    dims, mesh, fd = _load(args.input)
+    vr = float(fd.max() - fd.min())
+    thr, cnt = persistence_curve(_pairs(mesh, fd, "both", float("inf")), value_range=vr)
+    with open(args.output, "w") as fh:
+        json.dump([{"threshold": float(t), "count": int(c)} for t, c in zip(thr, cnt)], fh)
+    return 0
+
+
 def cmd_synth(ap, args) -> int:
     from .synthetic import CONFIGS, make_field
     if args.config not in CONFIGS:
@@ -166,7 +236,7 @@ def main(argv=None) -> int:
         p.add_argument("--preserve", help="vertex ids to preserve, one per line")
         p.add_argument("--keep-max", type=int, help="preserve the K highest maxima")
         p.add_argument("--keep-min", type=int, help="preserve the K lowest minima")
-        p.add_argument("--epsilon", help="persistence threshold (not in this build)")
+        p.add_argument("--epsilon", help="persistence threshold E or E%% of the value range")
         p.add_argument("--threads", help="accepted for compatibility; ignored")
 
     p = sub.add_parser("simplify")
@@ -186,14 +256,22 @@ def main(argv=None) -> int:
     p.add_argument("--input", required=True)
     p.add_argument("--repeat", type=int, default=5)
     selection(p)
+    p = sub.add_parser("diagram")
+    p.add_argument("--input", required=True)
+    p.add_argument("--output", required=True)
+    p.add_argument("--epsilon")
+    p.add_argument("--polarity", choices=["max", "min", "both"], default="both")
+    p = sub.add_parser("curve")
+    p.add_argument("--input", required=True)
+    p.add_argument("--output", required=True)
     p = sub.add_parser("synth")
     p.add_argument("--config", type=int, required=True)
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--output", required=True)
     args = ap.parse_args(argv)
     try:
-        return {"simplify": cmd_simplify, "verify": cmd_verify, "bench": cmd_bench,
-                "synth": cmd_synth}[args.cmd](ap, args)
+        return {"simplify": cmd_simplify, "verify": cmd_verify, "bench": cmd_bench, "diagram": cmd_diagram,
+                "curve": cmd_curve, "synth": cmd_synth}[args.cmd](ap, args)
     except (FieldError, MeshError, ConstraintNotExtremum, OSError) as e:
         print(f"error: {e}", file=sys.stderr)
         return 2

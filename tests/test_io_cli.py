@@ -64,7 +64,8 @@ def test_preserve_list():
 def test_cli_usage_errors(tmp_path):
     f = str(tmp_path / "f.sfg")
     open(f, "w").write("SFG 2 2 2\n0 1 2 3\n")
-    for argv in (["simplify", "--input", f, "--output", f + ".o", "--epsilon", "1%"],
+    for argv in (["bench", "--input", f, "--epsilon", "1%"],
+                 ["simplify", "--input", f, "--output", f + ".o", "--epsilon", "1%", "--preserve", f],
                  ["simplify", "--input", f, "--output", f + ".o"],
                  ["simplify", "--input", f, "--output", f + ".o", "--preserve", f, "--keep-max", "1",
                   "--keep-min", "1"],
@@ -115,3 +116,28 @@ def test_cli_simplify_verify_matches_oracle(tmp_path):
     np.save(order, G)
     assert cli.main(["verify", "--original", src, "--simplified", out, "--order", order,
                      "--preserve", plist]) == 1
+
+
+@pytest.mark.gpu
+def test_cli_persistence_commands(tmp_path):
+    """simplify --epsilon E% (persistence-driven), diagram and curve JSON."""
+    f = (np.round(np.random.default_rng(12).random((26, 30)) * 40) / 40).astype(np.float32)
+    dims = (30, 26)
+    src = str(tmp_path / "f.sfgb")
+    sio.write_field(src, dims, f.ravel())
+    out, rep, dia, cur = (str(tmp_path / x) for x in ("g.sfg", "r.json", "d.json", "c.json"))
+    assert cli.main(["simplify", "--input", src, "--epsilon", "20%", "--output", out, "--report", rep]) == 0
+    _, g = sio.read_field(out)
+    assert float(np.abs(g.astype(np.float64) - f.ravel()).max()) <= 0.2 * float(f.max() - f.min())
+    assert cli.main(["diagram", "--input", src, "--output", dia]) == 0
+    d = json.load(open(dia))
+    pol = {"MaxSaddle": 0, "MinSaddle": 0}
+    for e in d:
+        pol[e["polarity"]] += 1
+        if e["saddleVertex"] is not None:
+            assert e["persistence"] >= 0  # 0 only between tied values (quantised field)
+    glob = [e for e in d if e["saddleVertex"] is None]
+    assert len(glob) == 2  # epsilon = infinity: only the global pair survives per polarity
+    assert cli.main(["curve", "--input", src, "--output", cur]) == 0
+    c = json.load(open(cur))
+    assert c[0]["count"] == len(d) and all(a["count"] >= b["count"] for a, b in zip(c, c[1:]))
