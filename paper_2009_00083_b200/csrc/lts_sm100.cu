@@ -859,14 +859,17 @@ static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, i
   if (cnt > 0) {
     LTS_TRY(radix_sort((const uint32_t *)w.rtmp, (const uint32_t *)w.okey, cnt, bits_for(ni - 1), false, w.okey2,
                        w.oval, nullptr, w.sb, s));
-    const size_t shm = sizeof(int) * 2 * (size_t)nm;
-    const int use_smem = shm <= 200 * 1024;
+    // sorted forest edges gathered contiguously (ia/ib/ew slots are free now)
+    int *sa = w.buf0, *sb2 = w.buf1, *sw = w.buf2;
+    k_pn_gather<<<NB(cnt), 256, 0, s>>>(w.oval, cnt, ia, ib, ew, sa, sb2, sw);
+    const size_t shm = sizeof(int) * (size_t)nm;
+    const int use_smem = shm <= 220 * 1024;
     if (use_smem) LTS_CUDA(cudaFuncSetAttribute(k_pn_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_pn_sweep<<<1, 32, use_smem ? shm : 0, s>>>(w.oval, cnt, ia, ib, ew, nrank, nm, par, comp, use_smem,
-                                                 (int *)w.skey, (int *)w.sval);
+    k_pn_sweep<<<1, 256, use_smem ? shm : 0, s>>>(sa, sb2, sw, cnt, nrank, nm, par, use_smem, (int *)w.skey,
+                                                  (int *)w.sval);
     k_pn_pairs<<<NB(cnt), 256, 0, s>>>((const int *)w.skey, (const int *)w.sval, cnt, inv, rev, ni, f, eps, idx,
                                        pair);
-    g_launches += 2;
+    g_launches += 3;
   }
   k_pn_out<<<NB(nm), 256, 0, s>>>(w.ckey, pair, nm, ext_out, sad_out);
   g_launches++;

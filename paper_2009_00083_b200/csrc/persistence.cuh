@@ -15,7 +15,7 @@
 //      its edges can merge two components in Kruskal order);
 //   3. its edges sorted by weight (radix sort, descending);
 //   4. one sequential union-find sweep over those nm-1 edges with the Elder
-//      rule (union-find in shared memory when it fits, 8 B per maximum);
+//      rule (union-find in shared memory when it fits, 4 B per maximum);
 //   5. a parallel pass resolves vertices and applies the epsilon filter in
 //      float64, as the reference compares values (order.py:30-36 widens f).
 // The minima pairs run the same machinery on the reversed order.
@@ -115,33 +115,45 @@ __global__ void k_pn_mst_keys(const int *__restrict__ mst, const int *__restrict
   }
 }
 
-// Elder-rule sweep over the forest edges in decreasing weight: the younger
-// top of the two components dies at the junction.  One thread; the
-// union-find (parent, top rank) lives in shared memory when nm fits.
-__device__ __forceinline__ int pn_find(int *p, int x) {
-  while (p[x] != x) {
-    p[x] = p[p[x]];
-    x = p[x];
+// forest edges in sweep order, gathered into contiguous arrays so the
+// sequential sweep streams them instead of chasing edge ids
+__global__ void k_pn_gather(const uint32_t *__restrict__ order, int cnt, const int *__restrict__ ia,
+                            const int *__restrict__ ib, const int *__restrict__ ew, int *sa, int *sb, int *sw) {
+  GRID_STRIDE(k, cnt) {
+    const int e = (int)order[k];
+    sa[k] = ia[e];
+    sb[k] = ib[e];
+    sw[k] = ew[e];
   }
-  return x;
 }
 
-__global__ void k_pn_sweep(const uint32_t *__restrict__ order, int cnt, const int *__restrict__ ia,
-                           const int *__restrict__ ib, const int *__restrict__ ew,
-                           const int *__restrict__ nrank, int nm, int *gpar, int *gtop, int use_smem,
-                           int *young_r, int *junction_w) {
-  extern __shared__ int sh[];
-  if (threadIdx.x != 0) return;
-  int *par = use_smem ? sh : gpar;
-  int *top = use_smem ? sh + nm : gtop;
-  for (int i = 0; i < nm; i++) {
-    par[i] = i;
-    top[i] = nrank[i];
+// Elder-rule sweep over the forest edges in decreasing weight: the younger
+// top of the two components dies at the junction.  One thread.  The
+// union-find is one int per node: a non-negative entry is the parent, a root
+// holds -(top rank + 1); it lives in shared memory when nm fits (4 B per
+// extremum), else in global memory.
+__device__ __forceinline__ int pn_find(int *p, int x) {
+  for (;;) {
+    const int q = p[x];
+    if (q < 0) return x;  // x is a root
+    const int r = p[q];
+    if (r < 0) return q;  // q is the root
+    p[x] = r;             // path halving
+    x = r;
   }
+}
+
+__global__ void k_pn_sweep(const int *__restrict__ sa, const int *__restrict__ sb, const int *__restrict__ sw,
+                           int cnt, const int *__restrict__ nrank, int nm, int *gpar, int use_smem, int *young_r,
+                           int *junction_w) {
+  extern __shared__ int sh[];
+  int *par = use_smem ? sh : gpar;
+  for (int i = threadIdx.x; i < nm; i += blockDim.x) par[i] = -(nrank[i] + 1);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   for (int k = 0; k < cnt; k++) {
-    const int e = (int)order[k];
-    const int ra = pn_find(par, ia[e]), rb = pn_find(par, ib[e]);
-    const int ta = top[ra], tb = top[rb];
+    const int ra = pn_find(par, sa[k]), rb = pn_find(par, sb[k]);
+    const int ta = -par[ra] - 1, tb = -par[rb] - 1;
     // ranks are distinct: the lower top dies here, the union keeps the higher
     if (ta < tb) {
       young_r[k] = ta;
@@ -150,7 +162,7 @@ __global__ void k_pn_sweep(const uint32_t *__restrict__ order, int cnt, const in
       young_r[k] = tb;
       par[rb] = ra;
     }
-    junction_w[k] = ew[e];
+    junction_w[k] = sw[k];
   }
 }
 
