@@ -197,3 +197,18 @@ def test_edge_list_fallback_matches():
     env = dict(os.environ, LTS_FORCE_EDGE_LIST="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 4), (2, 3, 8), (3, 5, 12), (2, 33, 36), (70, 2, 64), (5, 40, 44),
+                                   (9, 9, 9), (2, 2, 2)])
+def test_simplify_small_3d_shapes(shape):
+    """Grid edges of the TMA classification path (x strips of 4, 32 x 32
+    columns, z chunks, out-of-grid halo cells) and of the fallback kernel
+    (nx not a multiple of 4), against the oracle."""
+    f = np.round(np.random.default_rng(sum(shape)).random(shape) * 20) / 20
+    dims, f32, pm, pn, ref = _oracle_case(np.asarray(f, np.float32), 3, 2)
+    mesh = _mesh(dims)
+    g, G, rep = P.simplify_field(mesh, _cu(f32), P.ConstraintSet(preserveMinima=pn, preserveMaxima=pm))
+    assert rep.ok == ref.ok
+    np.testing.assert_array_equal(G.rank32.cpu().numpy(), ref.G_rank)
+    assert g.values.cpu().numpy().tobytes() == ref.g.tobytes()
