@@ -67,7 +67,7 @@ __global__ void k_roots(const int *__restrict__ ptr, int64_t n, int *root) {
 // vertex class: 1 = discarded maximum (seed, in D), 2 = preserved maximum (P)
 __global__ void k_mark_maxima(const uint8_t *__restrict__ flags, const uint8_t *__restrict__ pmark,
                               int kind, int64_t n, uint8_t *vcls, uint8_t *cst, int *mlist,
-                              int *counts /* [0]=maxima [1]=D [2]=P */, int *comp, int *par,
+                              int *counts /* [0]=maxima [1]=D (one u64) */, int *comp, int *par,
                               int *acc, int *rpar, unsigned long long *bestP) {
   GRID_STRIDE(v, n) {
     uint8_t fl = flags[v];
@@ -82,10 +82,9 @@ __global__ void k_mark_maxima(const uint8_t *__restrict__ flags, const uint8_t *
     int lane = threadIdx.x & 31;
     int leader = __ffs(act) - 1;
     int base = 0;
-    if (lane == leader && mm) {
-      base = atomicAdd(counts, __popc(mm));
-      atomicAdd(counts + 1, __popc(md));
-      atomicAdd(counts + 2, __popc(mp));
+    if (lane == leader && mm) {  // one 64-bit atomic: D count high, all maxima low
+      const unsigned long long add = ((unsigned long long)__popc(md) << 32) | (unsigned)__popc(mm);
+      base = (int)(unsigned)(atomicAdd(reinterpret_cast<unsigned long long *>(counts), add) & 0xffffffffull);
     }
     base = __shfl_sync(act, base, leader);
     if (c) {

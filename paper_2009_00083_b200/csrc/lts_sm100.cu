@@ -188,7 +188,7 @@ struct WS {
 };
 
 enum {
-  SC_COUNTS = 0,   // 3
+  SC_COUNTS = 0,   // 2: all maxima, discarded maxima (one 64-bit counter)
   SC_ECOUNT = 4,
   SC_ACTIVE = 5,
   SC_ERR = 6,
@@ -481,8 +481,8 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
                                          w.scal + SC_COUNTS, w.comp, w.par, w.acc, w.rpar, w.bestP);
     g_launches++;
     LTS_KCHECK();
-    LTS_TRY(readback(c, SC_COUNTS, 3));
-    const int nm = c.h_scal[SC_COUNTS], nD = c.h_scal[SC_COUNTS + 1], nP = c.h_scal[SC_COUNTS + 2];
+    LTS_TRY(readback(c, SC_COUNTS, 2));
+    const int nm = c.h_scal[SC_COUNTS], nD = c.h_scal[SC_COUNTS + 1], nP = nm - nD;
     r.seeds = nD;
     if (nD == 0) {
       LTS_CUDA(cudaMemcpyAsync(new_rank, rank, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
@@ -782,7 +782,7 @@ static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, i
   k_roots<<<NB(n), 256, 0, s>>>(w.ptr, n, w.M);
   g_launches += 7;
   LTS_KCHECK();
-  LTS_TRY(readback(c, SC_COUNTS, 3));
+  LTS_TRY(readback(c, SC_COUNTS, 2));
   const int nm = c.h_scal[SC_COUNTS];
   *count_out = nm;
   if (nm == 0) return 0;
