@@ -21,10 +21,13 @@
 //     rank tau; regions = union-find over edges between claimed endpoints.
 // Parity with the reference sweep is checked in tests/test_gpu_parity.py.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "lts_common.cuh"
 #include "classify.cuh"  // Stencil
 
 namespace lts {
+namespace cg = cooperative_groups;
 
 extern int64_t g_launches;
 
@@ -450,18 +453,19 @@ __global__ void __launch_bounds__(ET_NT) k_edges_tile(Grid g, const int *__restr
 // ---- Boruvka rounds over the maxima graph --------------------------------
 
 
-__global__ void k_bv_reset(const int *__restrict__ mlist, int nm, unsigned long long *best) {
+__device__ __forceinline__ void bv_reset(int *mlist, int nm, unsigned long long *best) {
   GRID_STRIDE(i, nm) best[mlist[i]] = 0ull;
 }
+__global__ void k_bv_reset(int *mlist, int nm, unsigned long long *best) { bv_reset(mlist, nm, best); }
 
 // each thread scans a run of consecutive edges (edges are emitted per vertex,
 // so runs share endpoints) and only issues an atomic when its endpoint changes
 constexpr int BV_RUN = 8;
 // every active component starts a round from its members' heaviest edges
 // into preserved territory
-__global__ void k_bv_pmax(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
-                          const uint8_t *__restrict__ cst, const uint8_t *__restrict__ vcls,
-                          const unsigned long long *__restrict__ bestP, unsigned long long *best) {
+__device__ __forceinline__ void bv_pmax(int *mlist, int nm, int *comp,
+                          uint8_t *cst, uint8_t *vcls,
+                          unsigned long long *bestP, unsigned long long *best) {
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
     if (vcls[m] != 1) continue;
@@ -470,10 +474,13 @@ __global__ void k_bv_pmax(const int *__restrict__ mlist, int nm, const int *__re
     if (cst[c] == 0 && b) atomicMax(best + c, b);
   }
 }
+__global__ void k_bv_pmax(int *mlist, int nm, int *comp,
+                          uint8_t *cst, uint8_t *vcls,
+                          unsigned long long *bestP, unsigned long long *best) { bv_pmax(mlist, nm, comp, cst, vcls, bestP, best); }
 
-__global__ void k_bv_best(const int *__restrict__ ea, const int *__restrict__ eb,
-                          const int *__restrict__ ew, int ne, const int *__restrict__ comp,
-                          const uint8_t *__restrict__ cst, unsigned long long *best) {
+__device__ __forceinline__ void bv_best(int *ea, int *eb,
+                          int *ew, int ne, int *comp,
+                          uint8_t *cst, unsigned long long *best) {
   const int64_t nrun = ((int64_t)ne + BV_RUN - 1) / BV_RUN;
   GRID_STRIDE(r, nrun) {
     int64_t i0 = r * BV_RUN, i1 = min((int64_t)ne, i0 + BV_RUN);
@@ -500,10 +507,13 @@ __global__ void k_bv_best(const int *__restrict__ ea, const int *__restrict__ eb
     if (cur_b >= 0 && best_b) atomicMax(best + cur_b, best_b);
   }
 }
+__global__ void k_bv_best(int *ea, int *eb,
+                          int *ew, int ne, int *comp,
+                          uint8_t *cst, unsigned long long *best) { bv_best(ea, eb, ew, ne, comp, cst, best); }
 
 // active root: comp[m] == m && cst[m] == 0
-__global__ void k_bv_hook(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
-                          const uint8_t *__restrict__ cst, const unsigned long long *__restrict__ best,
+__device__ __forceinline__ void bv_hook(int *mlist, int nm, int *comp,
+                          uint8_t *cst, unsigned long long *best,
                           int *par, int *wc, int *err) {
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
@@ -519,9 +529,12 @@ __global__ void k_bv_hook(const int *__restrict__ mlist, int nm, const int *__re
     wc[m] = (int)(b >> 32) - 1;
   }
 }
+__global__ void k_bv_hook(int *mlist, int nm, int *comp,
+                          uint8_t *cst, unsigned long long *best,
+                          int *par, int *wc, int *err) { bv_hook(mlist, nm, comp, cst, best, par, wc, err); }
 
-__global__ void k_bv_cycle(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
-                           const uint8_t *__restrict__ cst, int *par) {
+__device__ __forceinline__ void bv_cycle(int *mlist, int nm, int *comp,
+                           uint8_t *cst, int *par) {
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
     if (comp[m] != m || cst[m] != 0) continue;
@@ -529,18 +542,22 @@ __global__ void k_bv_cycle(const int *__restrict__ mlist, int nm, const int *__r
     if (q != m && cst[q] == 0 && comp[q] == q && par[q] == m && m < q) par[m] = m;
   }
 }
+__global__ void k_bv_cycle(int *mlist, int nm, int *comp,
+                           uint8_t *cst, int *par) { bv_cycle(mlist, nm, comp, cst, par); }
 
-__global__ void k_bv_jump(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
-                          const uint8_t *__restrict__ cst, int *par) {
+__device__ __forceinline__ void bv_jump(int *mlist, int nm, int *comp,
+                          uint8_t *cst, int *par) {
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
     if (comp[m] != m || cst[m] != 0) continue;
     forest_root(par, m);
   }
 }
+__global__ void k_bv_jump(int *mlist, int nm, int *comp,
+                          uint8_t *cst, int *par) { bv_jump(mlist, nm, comp, cst, par); }
 
-__global__ void k_bv_roots(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
-                           const uint8_t *__restrict__ cst, const int *__restrict__ par, int *rt) {
+__device__ __forceinline__ void bv_roots(int *mlist, int nm, int *comp,
+                           uint8_t *cst, int *par, int *rt) {
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
     if (comp[m] != m || cst[m] != 0) continue;
@@ -549,12 +566,14 @@ __global__ void k_bv_roots(const int *__restrict__ mlist, int nm, const int *__r
     rt[m] = x;
   }
 }
+__global__ void k_bv_roots(int *mlist, int nm, int *comp,
+                           uint8_t *cst, int *par, int *rt) { bv_roots(mlist, nm, comp, cst, par, rt); }
 
 // members: tau accumulator and new component; comp is read through a snapshot
 // of the round's roots (par of the old root), so the update order is irrelevant
-__global__ void k_bv_members(const int *__restrict__ mlist, int nm, int *comp,
-                             const uint8_t *__restrict__ cst, const int *__restrict__ rt,
-                             const int *__restrict__ wc, int *acc) {
+__device__ __forceinline__ void bv_members(int *mlist, int nm, int *comp,
+                             uint8_t *cst, int *rt,
+                             int *wc, int *acc) {
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
     int c = comp[m];
@@ -564,10 +583,13 @@ __global__ void k_bv_members(const int *__restrict__ mlist, int nm, int *comp,
     comp[m] = rt[c];  // chain root of the old component (k_bv_roots)
   }
 }
+__global__ void k_bv_members(int *mlist, int nm, int *comp,
+                             uint8_t *cst, int *rt,
+                             int *wc, int *acc) { bv_members(mlist, nm, comp, cst, rt, wc, acc); }
 
 // after members moved: roots that reached preserved territory become final;
 // count remaining active roots (2-cycle roots)
-__global__ void k_bv_settle(const int *__restrict__ mlist, int nm, const int *__restrict__ comp,
+__device__ __forceinline__ void bv_settle(int *mlist, int nm, int *comp,
                             uint8_t *cst, int *active) {
   GRID_STRIDE(i, nm) {
     int m = mlist[i];
@@ -579,6 +601,52 @@ __global__ void k_bv_settle(const int *__restrict__ mlist, int nm, const int *__
       continue;
     }
     atomicAdd(active, 1);
+  }
+}
+__global__ void k_bv_settle(int *mlist, int nm, int *comp,
+                            uint8_t *cst, int *active) { bv_settle(mlist, nm, comp, cst, active); }
+
+// All Boruvka rounds in one cooperative launch: the phases of a round are
+// separated by grid-wide barriers instead of kernel boundaries, and the
+// "still active" test is read on the device instead of by a host readback per
+// round.  state[0] = active roots of the last round, state[1] = rounds run.
+struct BvArgs {
+  int *mlist;
+  int nm;
+  int *comp, *par, *wc, *rt, *acc, *err;
+  uint8_t *cst, *vcls;
+  unsigned long long *bestP, *best;
+  int *ea, *eb, *ew;
+  int ne;
+  int *state;
+};
+
+__global__ void __launch_bounds__(256) k_bv_coop(BvArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  for (int round = 0; round < 64; round++) {
+    bv_reset(a.mlist, a.nm, a.best);
+    if (lead) a.state[0] = 0;
+    grid.sync();
+    bv_pmax(a.mlist, a.nm, a.comp, a.cst, a.vcls, a.bestP, a.best);
+    if (a.ne > 0) bv_best(a.ea, a.eb, a.ew, a.ne, a.comp, a.cst, a.best);
+    grid.sync();
+    bv_hook(a.mlist, a.nm, a.comp, a.cst, a.best, a.par, a.wc, a.err);
+    grid.sync();
+    bv_cycle(a.mlist, a.nm, a.comp, a.cst, a.par);
+    grid.sync();
+    bv_jump(a.mlist, a.nm, a.comp, a.cst, a.par);
+    grid.sync();
+    bv_roots(a.mlist, a.nm, a.comp, a.cst, a.par, a.rt);
+    grid.sync();
+    bv_members(a.mlist, a.nm, a.comp, a.cst, a.rt, a.wc, a.acc);
+    grid.sync();
+    bv_settle(a.mlist, a.nm, a.comp, a.cst, a.state);
+    grid.sync();
+    const int act = *(volatile int *)a.state, bad = *(volatile int *)a.err;
+    if (lead) a.state[1] = round + 1;
+    if (act == 0 || bad) break;
+    grid.sync();  // every thread has read state[0] before the next round clears it
   }
 }
 

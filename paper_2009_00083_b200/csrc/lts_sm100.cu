@@ -209,6 +209,7 @@ enum {
   SC_BIGACT = 32,
   SC_BIGWORK = 34,  // 2 ints: 64-bit sum of region sizes flooded by k_big_flood
   SC_BIGSLOTS = 36, // = SC_NBIG + 7: slots of the big regions
+  SC_BVSTATE = 40,  // 2: active roots of the last Boruvka round, rounds run
   SC_N = 64
 };
 
@@ -538,25 +539,26 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     }
     const int ne = c.h_scal[SC_ECOUNT];
     r.maxima_edges = ne;
-    // Boruvka rounds: tau(m) = bottleneck to preserved maxima
-    for (int round = 0; round < 64; round++) {
-      k_bv_reset<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.best);
-      k_bv_pmax<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.vcls, w.bestP, w.best);
+    // Boruvka rounds: tau(m) = bottleneck to preserved maxima, all rounds in
+    // one cooperative launch (grid barriers between phases); one readback
+    {
+      static int coop_blocks = 0;
+      if (!coop_blocks) {
+        int dev = 0, nsm = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bv_coop, 256, 0);
+        coop_blocks = std::max(1, std::min(per, 4)) * nsm;
+      }
+      BvArgs ba{w.mlist, nm, w.comp, w.par, w.wc, w.rt, w.acc, w.scal + SC_ERR, w.cst, w.vcls, w.bestP, w.best,
+                ea, eb, ew, ne, w.scal + SC_BVSTATE};
+      void *kargs[] = {&ba};
+      LTS_CUDA(cudaLaunchCooperativeKernel((const void *)k_bv_coop, dim3(coop_blocks), dim3(256), kargs, 0, s));
       g_launches++;
-      if (ne > 0) k_bv_best<<<NB(ne), 256, 0, s>>>(ea, eb, ew, ne, w.comp, w.cst, w.best);
-      k_bv_hook<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.best, w.par, w.wc, w.scal + SC_ERR);
-      k_bv_cycle<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par);
-      k_bv_jump<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par);
-      k_bv_roots<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.par, w.rt);
-      k_bv_members<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.rt, w.wc, w.acc);
-      LTS_CUDA(cudaMemsetAsync(w.scal + SC_ACTIVE, 0, sizeof(int), s));
-      k_bv_settle<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.comp, w.cst, w.scal + SC_ACTIVE);
-      g_launches += 8;
       LTS_KCHECK();
-      LTS_TRY(readback(c, SC_ACTIVE, 2));
+      LTS_TRY(readback(c, SC_ERR, SC_BVSTATE + 2 - SC_ERR));
       if (c.h_scal[SC_ERR]) return lts_set_error(LTS_E_NO_SADDLE, "a discarded extremum cannot reach a preserved one");
-      r.boruvka_rounds = round + 1;
-      if (c.h_scal[SC_ACTIVE] == 0) break;
+      r.boruvka_rounds = c.h_scal[SC_BVSTATE + 1];
     }
     // regions: union-find over edges between claimed endpoints
     if (ne > 0) k_region_union<<<NB(ne), 256, 0, s>>>(ea, eb, ew, ne, w.vcls, w.acc, w.rpar);
