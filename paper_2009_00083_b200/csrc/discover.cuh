@@ -161,107 +161,11 @@ __global__ void k_hash_compact(EdgeHash H, int *ea, int *eb, int *ew, int *cnt) 
   }
 }
 
-// cross-manifold edges of the maxima graph.  Every grid edge is owned by its
+// Cross-manifold edges of the maxima graph.  Every grid edge is owned by its
 // lower endpoint u (weight = rank u), and u emits one edge per DISTINCT
 // neighbouring manifold: all of u's edges into the same manifold carry the
-// same weight, so the duplicates cannot change any bottleneck.  Output slots
-// are reserved with one global atomic per block iteration.
-template <int NDIM>
-__global__ void __launch_bounds__(256) k_edges(Grid g, const int *__restrict__ rank, int rev,
-                                               const int *__restrict__ M,
-                                               const uint8_t *__restrict__ vcls, int *ea, int *eb,
-                                               int *ew, int *ecount,
-                                               unsigned long long *bestP, EdgeHash H) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
-  __shared__ int s_w[8];
-  __shared__ int s_base;
-  const int n = (int)g.n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int v0 = blockIdx.x * blockDim.x; v0 < n; v0 += gridDim.x * blockDim.x) {
-    int v = v0 + threadIdx.x;
-    int bs[K];
-    int cnt = 0;
-    int a = 0, rv = 0;
-    if (v < n) {
-      int x, y, z;
-      coords(g, v, x, y, z);
-      a = M[v];
-      rv = eff_rank(rank, v, rev, n);
-      const bool pa = vcls[a] == 2;
-#pragma unroll
-      for (int k = 0; k < K; k++) {
-        int u = nbr_at(g, x, y, z, k);
-        if (u < 0 || eff_rank(rank, u, rev, n) < rv) continue;  // owned by u
-        int b = M[u];
-        if (b == a || (pa && vcls[b] == 2)) continue;
-        bool dup = false;
-#pragma unroll
-        for (int i = 0; i < K; i++)
-          if (i < cnt && bs[i] == b) dup = true;
-        if (!dup) bs[cnt++] = b;
-      }
-    }
-    // warp-level de-duplication: lanes (consecutive vertices) that emit the
-    // same manifold pair keep only the heaviest edge (highest lower endpoint)
-    unsigned keep = 0;
-#pragma unroll
-    for (int i = 0; i < K; i++) {
-      const bool has = i < cnt;
-      if (__ballot_sync(0xffffffffu, has) == 0) break;
-      const unsigned long long key = has ? (((unsigned long long)(unsigned)a << 32) | (unsigned)bs[i]) : ~0ull;
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
-      const int best = __reduce_max_sync(peers, has ? rv : -1);
-      // the lane holding the heaviest copy emits (ranks are distinct).  An
-      // edge between a discarded and a preserved manifold only ever matters
-      // as the discarded side's heaviest edge into preserved territory: it is
-      // folded into bestP[discarded] instead of being emitted.
-      if (has && rv == best) {
-        const bool pa = vcls[a] == 2, pb = vcls[bs[i]] == 2;
-        if (pa != pb) {
-          const int d = pa ? bs[i] : a, pm = pa ? a : bs[i];
-          atomicMax(bestP + d, bv_pack(rv, pm));
-        } else if (H.bits) {
-          eh_insert(H, a, bs[i], rv);
-        } else {
-          keep |= 1u << i;
-        }
-      }
-    }
-    if (H.bits) continue;  // block-uniform
-    int kc = __popc(keep);
-    int incl = kc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int acc = 0;
-      for (int i = 0; i < 8; i++) {
-        int t = s_w[i];
-        s_w[i] = acc;
-        acc += t;
-      }
-      s_base = acc ? atomicAdd(ecount, acc) : 0;
-    }
-    __syncthreads();
-    int slot = s_base + s_w[warp] + incl - kc;
-#pragma unroll
-    for (int i = 0; i < K; i++)
-      if (keep >> i & 1u) {
-        ea[slot] = a;
-        eb[slot] = bs[i];
-        ew[slot] = rv;
-        slot++;
-      }
-    __syncthreads();
-  }
-}
-
-// Tiled form of k_edges.  A CTA owns a 32 x 8 (x, y) column of the grid and
-// marches in z (one z plane for 2D grids); the manifold labels M and the
+// same weight, so the duplicates cannot change any bottleneck.  A CTA owns a
+// 32 x 8 (x, y) column of the grid and marches in z (one z plane for 2D grids); the manifold labels M and the
 // ranks of planes z-1..z+1 sit in a 5-slot shared-memory ring with halo, so
 // the 14-neighbour tests never touch L1/L2.  Edges found by the CTA are
 // combined in a shared hash table (one slot per manifold pair, heaviest
@@ -456,7 +360,6 @@ __global__ void __launch_bounds__(ET_NT) k_edges_tile(Grid g, const int *__restr
 __device__ __forceinline__ void bv_reset(int *mlist, int nm, unsigned long long *best) {
   GRID_STRIDE(i, nm) best[mlist[i]] = 0ull;
 }
-__global__ void k_bv_reset(int *mlist, int nm, unsigned long long *best) { bv_reset(mlist, nm, best); }
 
 // each thread scans a run of consecutive edges (edges are emitted per vertex,
 // so runs share endpoints) and only issues an atomic when its endpoint changes
@@ -474,9 +377,6 @@ __device__ __forceinline__ void bv_pmax(int *mlist, int nm, int *comp,
     if (cst[c] == 0 && b) atomicMax(best + c, b);
   }
 }
-__global__ void k_bv_pmax(int *mlist, int nm, int *comp,
-                          uint8_t *cst, uint8_t *vcls,
-                          unsigned long long *bestP, unsigned long long *best) { bv_pmax(mlist, nm, comp, cst, vcls, bestP, best); }
 
 __device__ __forceinline__ void bv_best(int *ea, int *eb,
                           int *ew, int ne, int *comp,
@@ -507,9 +407,6 @@ __device__ __forceinline__ void bv_best(int *ea, int *eb,
     if (cur_b >= 0 && best_b) atomicMax(best + cur_b, best_b);
   }
 }
-__global__ void k_bv_best(int *ea, int *eb,
-                          int *ew, int ne, int *comp,
-                          uint8_t *cst, unsigned long long *best) { bv_best(ea, eb, ew, ne, comp, cst, best); }
 
 // active root: comp[m] == m && cst[m] == 0
 __device__ __forceinline__ void bv_hook(int *mlist, int nm, int *comp,
@@ -529,9 +426,6 @@ __device__ __forceinline__ void bv_hook(int *mlist, int nm, int *comp,
     wc[m] = (int)(b >> 32) - 1;
   }
 }
-__global__ void k_bv_hook(int *mlist, int nm, int *comp,
-                          uint8_t *cst, unsigned long long *best,
-                          int *par, int *wc, int *err) { bv_hook(mlist, nm, comp, cst, best, par, wc, err); }
 
 __device__ __forceinline__ void bv_cycle(int *mlist, int nm, int *comp,
                            uint8_t *cst, int *par) {
@@ -542,8 +436,6 @@ __device__ __forceinline__ void bv_cycle(int *mlist, int nm, int *comp,
     if (q != m && cst[q] == 0 && comp[q] == q && par[q] == m && m < q) par[m] = m;
   }
 }
-__global__ void k_bv_cycle(int *mlist, int nm, int *comp,
-                           uint8_t *cst, int *par) { bv_cycle(mlist, nm, comp, cst, par); }
 
 __device__ __forceinline__ void bv_jump(int *mlist, int nm, int *comp,
                           uint8_t *cst, int *par) {
@@ -553,8 +445,6 @@ __device__ __forceinline__ void bv_jump(int *mlist, int nm, int *comp,
     forest_root(par, m);
   }
 }
-__global__ void k_bv_jump(int *mlist, int nm, int *comp,
-                          uint8_t *cst, int *par) { bv_jump(mlist, nm, comp, cst, par); }
 
 __device__ __forceinline__ void bv_roots(int *mlist, int nm, int *comp,
                            uint8_t *cst, int *par, int *rt) {
@@ -566,8 +456,6 @@ __device__ __forceinline__ void bv_roots(int *mlist, int nm, int *comp,
     rt[m] = x;
   }
 }
-__global__ void k_bv_roots(int *mlist, int nm, int *comp,
-                           uint8_t *cst, int *par, int *rt) { bv_roots(mlist, nm, comp, cst, par, rt); }
 
 // members: tau accumulator and new component; comp is read through a snapshot
 // of the round's roots (par of the old root), so the update order is irrelevant
@@ -580,12 +468,9 @@ __device__ __forceinline__ void bv_members(int *mlist, int nm, int *comp,
     if (cst[c] != 0) continue;  // preserved or already final
     int w = wc[c];
     if (w < acc[m]) acc[m] = w;
-    comp[m] = rt[c];  // chain root of the old component (k_bv_roots)
+    comp[m] = rt[c];  // chain root of the old component (bv_roots)
   }
 }
-__global__ void k_bv_members(int *mlist, int nm, int *comp,
-                             uint8_t *cst, int *rt,
-                             int *wc, int *acc) { bv_members(mlist, nm, comp, cst, rt, wc, acc); }
 
 // after members moved: roots that reached preserved territory become final;
 // count remaining active roots (2-cycle roots)
@@ -603,8 +488,6 @@ __device__ __forceinline__ void bv_settle(int *mlist, int nm, int *comp,
     atomicAdd(active, 1);
   }
 }
-__global__ void k_bv_settle(int *mlist, int nm, int *comp,
-                            uint8_t *cst, int *active) { bv_settle(mlist, nm, comp, cst, active); }
 
 // All Boruvka rounds in one cooperative launch: the phases of a round are
 // separated by grid-wide barriers instead of kernel boundaries, and the
