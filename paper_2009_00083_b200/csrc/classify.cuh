@@ -96,7 +96,6 @@ __device__ __forceinline__ void classify_pair(const int *__restrict__ p0, const 
                                               int16_t *__restrict__ lower, int16_t *__restrict__ upper,
                                               const uint8_t *__restrict__ lut, int32_t *__restrict__ ptr) {
   using St = Stencil<NDIM>;
-  constexpr int K = St::K;
   constexpr int CP_PITCH = PITCH;
   {
       // plane z rows y-1, y, y+1
@@ -246,7 +245,6 @@ __global__ void __launch_bounds__(CP_TX *CP_TY) k_classify_tile(Grid g, const in
                                                              const uint8_t *__restrict__ lut,
                                                              int32_t *__restrict__ ptr) {
   using St = Stencil<NDIM>;
-  constexpr int K = St::K;
   constexpr int NP = NDIM == 2 ? 1 : CP_RING;
   __shared__ __align__(16) int pl[NP][CP_ROWS * CP_PITCH];
   const int tid = threadIdx.y * CP_TX + threadIdx.x;
