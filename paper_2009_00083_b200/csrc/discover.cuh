@@ -165,14 +165,20 @@ __global__ void k_hash_compact(EdgeHash H, int *ea, int *eb, int *ew, int *cnt) 
 // lower endpoint u (weight = rank u), and u emits one edge per DISTINCT
 // neighbouring manifold: all of u's edges into the same manifold carry the
 // same weight, so the duplicates cannot change any bottleneck.  A CTA owns a
-// 32 x 8 (x, y) column of the grid and marches in z (one z plane for 2D grids); the manifold labels M and the
+// 32 x 16 (x, y) column of the grid and marches in z (8-plane chunks) (one z plane for 2D grids); the manifold labels M and the
 // ranks of planes z-1..z+1 sit in a 5-slot shared-memory ring with halo, so
 // the 14-neighbour tests never touch L1/L2.  Edges found by the CTA are
 // combined in a shared hash table (one slot per manifold pair, heaviest
 // weight) and flushed to the global table / bestP once it fills and at the
 // end: a manifold boundary crossing the tile costs one global update instead
 // of one per boundary vertex.
-constexpr int ET_TX = 32, ET_TY = 8, ET_ZC = 16, ET_RING = 5;
+#ifndef LTS_ET_ZC
+#define LTS_ET_ZC 8
+#endif
+#ifndef LTS_ET_TY
+#define LTS_ET_TY 16
+#endif
+constexpr int ET_TX = 32, ET_TY = LTS_ET_TY, ET_ZC = LTS_ET_ZC, ET_RING = 5;
 constexpr int ET_PX = ET_TX + 2, ET_PY = ET_TY + 2, ET_PL = ET_PX * ET_PY;
 constexpr int ET_NT = ET_TX * ET_TY, ET_NEPT = (ET_PL + ET_NT - 1) / ET_NT;
 constexpr int ET_HT = 2048, ET_FLUSH = 1024;  // shared table slots / flush level
