@@ -628,7 +628,10 @@ __device__ __forceinline__ bool claimed_bit(const uint32_t *cbits, int v) {
 // and a decoupled look-back over the tiles' published counts gives the tile's
 // output offset (replaces flags + a three-kernel scan + compaction).
 // st[0] = tile ticket counter, st[1 + tile] = status (2 flag bits | count).
-constexpr int CC_T = 256, CC_IPT = 16, CC_TILE = CC_T * CC_IPT;
+#ifndef LTS_CC_IPT
+#define LTS_CC_IPT 8
+#endif
+constexpr int CC_T = 256, CC_IPT = LTS_CC_IPT, CC_TILE = CC_T * CC_IPT;
 constexpr int CC_AGG = 1 << 30, CC_PRE = 2 << 30, CC_VAL = (1 << 30) - 1;
 
 __global__ void __launch_bounds__(CC_T) k_claimed_compact_lb(const int *__restrict__ inv, int rev, int n,

@@ -31,6 +31,9 @@
 namespace lts {
 int64_t g_launches = 0;
 }
+#ifndef LTS_BV_COOP_PER_SM
+#define LTS_BV_COOP_PER_SM 1
+#endif
 
 using namespace lts;
 
@@ -548,7 +551,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bv_coop, 256, 0);
-        coop_blocks = std::max(1, std::min(per, 4)) * nsm;
+        coop_blocks = std::max(1, std::min(per, LTS_BV_COOP_PER_SM)) * nsm;
       }
       BvArgs ba{w.mlist, nm, w.comp, w.par, w.wc, w.rt, w.acc, w.scal + SC_ERR, w.cst, w.vcls, w.bestP, w.best,
                 ea, eb, ew, ne, w.scal + SC_BVSTATE};
