@@ -31,6 +31,9 @@
 namespace lts {
 int64_t g_launches = 0;
 }
+#ifndef LTS_JUMPS
+#define LTS_JUMPS 3  // pointer-jumping launches on the ascent forest before path halving
+#endif
 #ifndef LTS_BV_COOP_PER_SM
 #define LTS_BV_COOP_PER_SM 1
 #endif
@@ -496,7 +499,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       return 0;
     }
     if (nP == 0) return lts_set_error(LTS_E_NO_SADDLE, "every extremum of this kind is discarded: no saddle");
-    for (int j = 0; j < 3; j++) k_jump<<<NB(n), 256, 0, s>>>(w.ptr, n);
+    for (int j = 0; j < LTS_JUMPS; j++) k_jump<<<NB(n), 256, 0, s>>>(w.ptr, n);
     k_compress<<<NB(n), 256, 0, s>>>(w.ptr, n);
     k_roots<<<NB(n), 256, 0, s>>>(w.ptr, n, w.M);
     g_launches += 3;
@@ -782,7 +785,7 @@ static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, i
   launch_classify(c.g, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
   k_mark_maxima<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, kind, n, w.vcls, w.cst, w.mlist, w.scal + SC_COUNTS,
                                        w.comp, w.par, w.acc, w.rpar, w.bestP);
-  for (int j = 0; j < 3; j++) k_jump<<<NB(n), 256, 0, s>>>(w.ptr, n);
+  for (int j = 0; j < LTS_JUMPS; j++) k_jump<<<NB(n), 256, 0, s>>>(w.ptr, n);
   k_compress<<<NB(n), 256, 0, s>>>(w.ptr, n);
   k_roots<<<NB(n), 256, 0, s>>>(w.ptr, n, w.M);
   g_launches += 7;
