@@ -632,7 +632,7 @@ __device__ __forceinline__ bool claimed_bit(const uint32_t *cbits, int v) {
 #define LTS_CC_IPT 8
 #endif
 constexpr int CC_T = 256, CC_IPT = LTS_CC_IPT, CC_TILE = CC_T * CC_IPT;
-constexpr int CC_AGG = 1 << 30, CC_PRE = 2 << 30, CC_VAL = (1 << 30) - 1;
+constexpr int CC_AGG = 1 << 30, CC_PRE = (int)(2u << 30), CC_VAL = (1 << 30) - 1;
 
 __global__ void __launch_bounds__(CC_T) k_claimed_compact_lb(const int *__restrict__ inv, int rev, int n,
                                                            const uint32_t *__restrict__ cbits,
@@ -668,26 +668,37 @@ __global__ void __launch_bounds__(CC_T) k_claimed_compact_lb(const int *__restri
     pre += w < warp ? x : 0;
     tot += x;
   }
-  if (tid == 0) {
+  if (warp == 0) {
+    // decoupled look-back, 32 predecessors per round trip: publish the tile
+    // aggregate, then sum predecessors back to the nearest inclusive prefix
     volatile int *S = st + 1;
     int base = 0;
     if (tile == 0) {
-      S[0] = CC_PRE | tot;
+      if (lane == 0) S[0] = CC_PRE | tot;
     } else {
-      S[tile] = CC_AGG | tot;
+      if (lane == 0) S[tile] = CC_AGG | tot;
       int acc = 0;
-      for (int64_t p = tile - 1; p >= 0;) {
-        const int sv = S[p];
-        if ((sv & ~CC_VAL) == 0) continue;  // predecessor not published yet
-        acc += sv & CC_VAL;
-        if ((sv & ~CC_VAL) == CC_PRE) break;
-        p--;
+      int64_t hi = (int64_t)tile - 1;  // newest predecessor of the window
+      for (;;) {
+        const int64_t p = hi - lane;
+        const int sv = p >= 0 ? (int)S[p] : (int)CC_PRE;
+        const int flag = sv & ~CC_VAL;
+        if (__any_sync(0xffffffffu, flag == 0)) continue;  // someone in the window has not published
+        const unsigned pre_mask = __ballot_sync(0xffffffffu, flag == CC_PRE);
+        const int stop = pre_mask ? __ffs(pre_mask) - 1 : 31;  // nearest inclusive prefix
+        int v = lane <= stop ? (sv & CC_VAL) : 0;
+        v = __reduce_add_sync(0xffffffffu, v);
+        acc += v;
+        if (pre_mask) break;
+        hi -= 32;
       }
       base = acc;
-      S[tile] = CC_PRE | (acc + tot);
+      if (lane == 0) S[tile] = CC_PRE | (acc + tot);
     }
-    s_base = base;
-    if ((int64_t)(tile + 1) * CC_TILE >= n) *total = base + tot;
+    if (lane == 0) {
+      s_base = base;
+      if ((int64_t)(tile + 1) * CC_TILE >= n) *total = base + tot;
+    }
   }
   __syncthreads();
   int p = s_base + pre + inc - c;
