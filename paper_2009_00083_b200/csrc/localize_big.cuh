@@ -41,7 +41,10 @@ constexpr int BIG_CHUNK = BIG_T * BIG_WPT;    // leaf words per scan chunk
 constexpr int BIG_CHUNK_SHIFT = BIG_CHUNK == 512 ? 14 : BIG_CHUNK == 1024 ? 15 : BIG_CHUNK == 2048 ? 16 : 17;
 static_assert((32 * BIG_CHUNK) == (1 << BIG_CHUNK_SHIFT), "chunk = BIG_CHUNK leaf words");
 constexpr int BIG_SMEM_WORDS = 16 * 1024;     // bit-set words in shared memory (rest of the SM is L1)
-constexpr int BIG_THRESHOLD = 256;            // regions with k > this use this kernel
+#ifndef LTS_BIG_THRESHOLD
+#define LTS_BIG_THRESHOLD 256
+#endif
+constexpr int BIG_THRESHOLD = LTS_BIG_THRESHOLD;  // regions with k > this use this kernel
 
 struct BigArgs {
   int *v0;           // per big region: first admissible boundary minimum
