@@ -31,6 +31,9 @@
 namespace lts {
 int64_t g_launches = 0;
 }
+#ifndef LTS_PEEL_ROUNDS
+#define LTS_PEEL_ROUNDS 16  // leaf-peeling rounds of the persistence forest before the sweep
+#endif
 #ifndef LTS_JUMPS
 #define LTS_JUMPS 3  // pointer-jumping launches on the ascent forest before path halving
 #endif
@@ -865,19 +868,46 @@ static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, i
     cnt = c.h_scal[SC_TMP];
   }
   if (cnt > 0) {
-    LTS_TRY(radix_sort((const uint32_t *)w.rtmp, (const uint32_t *)w.okey, cnt, bits_for(ni - 1), false, w.okey2,
-                       w.oval, nullptr, w.sb, s));
-    // sorted forest edges gathered contiguously (ia/ib/ew slots are free now)
-    int *sa = w.buf0, *sb2 = w.buf1, *sw = w.buf2;
-    k_pn_gather<<<NB(cnt), 256, 0, s>>>(w.oval, cnt, ia, ib, ew, sa, sb2, sw);
-    const size_t shm = sizeof(int) * (size_t)nm;
-    const int use_smem = shm <= 220 * 1024;
-    if (use_smem) LTS_CUDA(cudaFuncSetAttribute(k_pn_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_pn_sweep<<<1, 256, use_smem ? shm : 0, s>>>(sa, sb2, sw, cnt, nrank, nm, par, use_smem, (int *)w.skey,
-                                                  (int *)w.sval);
+    // leaf peeling: leaves lower than their only neighbour die at that edge
+    int *pa = w.buf0, *pb = w.buf1, *pw = w.buf2;
+    int *alive = w.flagscan, *deg = w.ridx, *deg0 = w.reg_of, *map = w.loc_of, *nrank2 = w.wc;
+    LTS_CUDA(cudaMemsetAsync(deg, 0, sizeof(int) * (size_t)nm, s));
+    LTS_CUDA(cudaMemsetAsync(w.scal + SC_BVSTATE, 0, sizeof(int) * 2, s));
+    k_pn_leaf_init<<<NB(cnt), 256, 0, s>>>((const uint32_t *)w.okey, cnt, ia, ib, ew, pa, pb, pw, alive, deg);
+    g_launches++;
+    for (int round = 0; round < LTS_PEEL_ROUNDS; round++) {
+      k_pn_copy<<<NB(nm), 256, 0, s>>>(deg, nm, deg0);
+      k_pn_peel<<<NB(cnt), 256, 0, s>>>(pa, pb, pw, cnt, nrank, deg0, deg, alive, (int *)w.skey, (int *)w.sval,
+                                        w.scal + SC_BVSTATE);
+      g_launches += 2;
+    }
+    LTS_KCHECK();
+    LTS_TRY(readback(c, SC_BVSTATE, 1));
+    const int rem = cnt - c.h_scal[SC_BVSTATE];
+    if (rem > 0) {
+      // the rest by the sequential Elder-rule sweep, in decreasing weight
+      LTS_CUDA(cudaMemsetAsync(w.scal + SC_TMP, 0, sizeof(int), s));
+      k_pn_rest_keys<<<NB(cnt), 256, 0, s>>>(alive, pw, cnt, ni, (uint32_t *)w.rtmp, (uint32_t *)w.okey,
+                                             w.scal + SC_TMP);
+      k_pn_remap<<<NB(nm), 256, 0, s>>>(deg, nm, nrank, map, nrank2, w.scal + SC_BVSTATE + 1);
+      g_launches += 2;
+      LTS_TRY(readback(c, SC_BVSTATE, 2));
+      const int nm2 = c.h_scal[SC_BVSTATE + 1];
+      LTS_TRY(radix_sort((const uint32_t *)w.rtmp, (const uint32_t *)w.okey, rem, bits_for(ni - 1), false,
+                         w.okey2, w.oval, nullptr, w.sb, s));
+      int *sa = w.verts, *sb2 = w.out, *sw = (int *)w.gheap;
+      k_pn_gather_rest<<<NB(rem), 256, 0, s>>>(w.oval, rem, pa, pb, pw, map, sa, sb2, sw);
+      const size_t shm = sizeof(int) * (size_t)nm2;
+      const int use_smem = shm <= 220 * 1024;
+      if (use_smem)
+        LTS_CUDA(cudaFuncSetAttribute(k_pn_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+      k_pn_sweep<<<1, 256, use_smem ? shm : 0, s>>>(sa, sb2, sw, rem, nrank2, nm2, par, use_smem, (int *)w.skey,
+                                                    (int *)w.sval);
+      g_launches += 2;
+    }
     k_pn_pairs<<<NB(cnt), 256, 0, s>>>((const int *)w.skey, (const int *)w.sval, cnt, inv, rev, ni, f, eps, idx,
                                        pair);
-    g_launches += 3;
+    g_launches++;
   }
   k_pn_out<<<NB(nm), 256, 0, s>>>(w.ckey, pair, nm, ext_out, sad_out);
   g_launches++;

@@ -166,6 +166,87 @@ __global__ void k_pn_sweep(const int *__restrict__ sa, const int *__restrict__ s
   }
 }
 
+// ---- leaf peeling of the spanning forest (before the sequential sweep) ----
+// A forest leaf m whose only remaining edge e leads to a higher node dies at
+// e in Kruskal order, whatever the order: its component is m (plus lower,
+// already peeled nodes) until e, and e joins it to a component whose top is
+// at least the neighbour.  Removing m and e changes no other pairing.  Rounds
+// of this run in parallel; the sweep then handles the rest.  Pair entries of
+// peeled leaves fill the (young rank, junction) list from the back.
+__global__ void k_pn_leaf_init(const uint32_t *__restrict__ order, int cnt, const int *__restrict__ ia,
+                               const int *__restrict__ ib, const int *__restrict__ ew, int *pa, int *pb, int *pw,
+                               int *alive, int *deg) {
+  GRID_STRIDE(k, cnt) {
+    const int e = (int)order[k];
+    const int a = ia[e], b = ib[e];
+    pa[k] = a;
+    pb[k] = b;
+    pw[k] = ew[e];
+    alive[k] = 1;
+    atomicAdd(deg + a, 1);
+    atomicAdd(deg + b, 1);
+  }
+}
+
+__global__ void k_pn_copy(const int *__restrict__ src, int nm, int *dst) {
+  GRID_STRIDE(i, nm) dst[i] = src[i];
+}
+
+__global__ void k_pn_peel(const int *__restrict__ pa, const int *__restrict__ pb, const int *__restrict__ pw,
+                          int cnt, const int *__restrict__ nrank, const int *__restrict__ deg0, int *deg,
+                          int *alive, int *young_r, int *junction_w, int *npeeled) {
+  GRID_STRIDE(k, cnt) {
+    if (!alive[k]) continue;
+    const int a = pa[k], b = pb[k];
+    const int ra = nrank[a], rb = nrank[b];
+    int leaf = -1, other = -1, r = 0;
+    if (deg0[a] == 1 && ra < rb) leaf = a, other = b, r = ra;
+    else if (deg0[b] == 1 && rb < ra) leaf = b, other = a, r = rb;
+    if (leaf < 0) continue;
+    alive[k] = 0;
+    atomicSub(deg + other, 1);
+    const int slot = cnt - 1 - atomicAdd(npeeled, 1);
+    young_r[slot] = r;
+    junction_w[slot] = pw[k];
+  }
+}
+
+// remaining forest edges: sort keys, and compact node numbering for the sweep
+__global__ void k_pn_rest_keys(const int *__restrict__ alive, const int *__restrict__ pw, int cnt, int n,
+                               uint32_t *key, uint32_t *val, int *count) {
+  GRID_STRIDE(k, cnt) {
+    const bool on = alive[k] != 0;
+    const int slot = warp_alloc(count, on);
+    if (on) {
+      key[slot] = (uint32_t)(n - 1 - pw[k]);
+      val[slot] = (uint32_t)k;
+    }
+  }
+}
+
+__global__ void k_pn_remap(const int *__restrict__ deg, int nm, const int *__restrict__ nrank, int *map, int *nrank2,
+                           int *count) {
+  GRID_STRIDE(i, nm) {
+    const bool on = deg[i] > 0;
+    const int slot = warp_alloc(count, on);
+    if (on) {
+      map[i] = slot;
+      nrank2[slot] = nrank[i];
+    }
+  }
+}
+
+__global__ void k_pn_gather_rest(const uint32_t *__restrict__ order, int rem, const int *__restrict__ pa,
+                                 const int *__restrict__ pb, const int *__restrict__ pw, const int *__restrict__ map,
+                                 int *sa, int *sb, int *sw) {
+  GRID_STRIDE(k, rem) {
+    const int e = (int)order[k];
+    sa[k] = map[pa[e]];
+    sb[k] = map[pb[e]];
+    sw[k] = pw[e];
+  }
+}
+
 // vertices of the young tops and junctions; epsilon filter in float64
 // (values[top] - values[junction] < eps, _kernels.py:390-393 / 406-408)
 __global__ void k_pn_pairs(const int *__restrict__ young_r, const int *__restrict__ junction_w, int cnt,
