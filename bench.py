@@ -13,12 +13,17 @@ field of BASELINE config 3, inputs resident in HBM.  Prints ONE JSON line.
          H2D of f + preserve lists, D2H of g and G, inside the timed region
   roofline  dominant kernel of the step vs MEASURED_PEAKS.json HBM GB/s
   cpu_baseline  the CPU oracle (C port of the reference kernels + SPEC glue)
-         on a bounded z-slab sample of the same field, rank 0 only
+         running the same full pass on the same field (rank 0 only), with
+         the host CPU model and the threads used
+  configs  one warm-up + one timed full pass of each other BASELINE config
+         (cfg1, cfg2, cfg4, cfg5), with their parity against the oracle
+         digests of tests/golden/full_hashes.json
 
 --impl reference runs the CPU oracle port (the reference is Python/numba and
-does not travel to the GPU box) on that sample per step.
+does not travel to the GPU box) on the same full pass per step.
 Multi-GPU: one process per GPU (torchrun), independent replicas
-("replicas only"): the path has no data exchange.
+("replicas only"): the path has no data exchange.  `--gpus N`
+without torchrun re-launches itself under torch.distributed.run.
 """
 from __future__ import annotations
 
@@ -106,20 +111,26 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample(f3d: np.ndarray, cfg, nz: int):
-    """Bounded sample of the workload for the CPU baseline: the first nz
-    z-planes of the same field, preserve counts scaled by nz/NZ."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_workload(f3d: np.ndarray, cfg):
+    """The benchmark's own workload for the CPU legs: the full field and the
+    same preserve lists (top-K maxima / bottom-K minima of F)."""
     from paper_2009_00083_b200 import synthetic as S
     from oracle import lts_oracle as O
-    sub = np.ascontiguousarray(f3d[:nz])
-    dims = tuple(sub.shape[::-1])
-    fr = sub.ravel()
+    dims = tuple(f3d.shape[::-1])
+    fr = np.ascontiguousarray(f3d.ravel())
     rank, _ = O.order_field(fr)
     mn, mx = O.extrema(dims, rank, os.cpu_count())
-    scale = nz / f3d.shape[0]
-    kmax = max(1, int(round(cfg.n_keep_max * scale)))
-    kmin = max(1, int(round(cfg.n_keep_min * scale)))
-    pm, pn = S.select_preserved(rank, mx, mn, kmax, kmin)
+    pm, pn = S.select_preserved(rank, mx, mn, cfg.n_keep_max, cfg.n_keep_min)
     return dims, fr, pm, pn
 
 
@@ -132,34 +143,101 @@ def run_oracle(dims, fr, pm, pn, threads):
     return dt
 
 
+def workload_config(cfg, args, n, npres, world):
+    """The `config` object both arms print (same workload, same keys)."""
+    return {"workload": f"{cfg.name} full LTS pass", "grid": list(cfg.dims), "n": n, "seed": args.seed,
+            "preserve": [int(npres[0]), int(npres[1])],
+            "parallelism": "replicas" if world > 1 else "single",
+            "l2": "flushed between steps (256 MiB write, outside the per-step events)"}
+
+
 def reference_arm(args):
+    """The reference's CPU path (the pinned C port of its numba kernels + the
+    SPEC glue, oracle/) on the SAME workload as our arm: the full cfg3 pass
+    over the whole 256^3 field with the same preserve lists, every host
+    thread (OpenMP where the reference uses prange; discover, sort and the
+    realisation sweep are sequential as in the reference).  The C port has no
+    JIT, so one untimed pass stands in for the warm-up steps."""
     rank, world, local = dist_env()
     if rank != 0:
         return
     from paper_2009_00083_b200 import synthetic as S
     cfg = S.CONFIGS[args.config]
     f3d = S.make_field(args.config, args.seed)
-    nz = args.cpu_nz
-    dims, fr, pm, pn = cpu_sample(f3d, cfg, nz)
+    dims, fr, pm, pn = cpu_workload(f3d, cfg)
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
+    if args.warmup > 0:
         run_oracle(dims, fr, pm, pn, threads)
     ts = [run_oracle(dims, fr, pm, pn, threads) for _ in range(args.steps)]
     t = sum(ts) / len(ts)
     v = fr.size / t
-    sample = (f"first {nz} z-planes of the {cfg.name} field (seed {args.seed}), {fr.size} voxels, "
-              f"preserve {pm.size} max / {pn.size} min; full pass per step")
+    sample = (f"the full workload: {cfg.name} field (seed {args.seed}), {fr.size} voxels, "
+              f"preserve {pm.size} max / {pn.size} min, one full LTS pass per step "
+              f"({t:.1f} s each); host CPU {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} full LTS pass", "grid": list(cfg.dims), "seed": args.seed,
-                   "sample_grid": list(dims)},
+        "config": workload_config(cfg, args, fr.size, (pm.size, pn.size), world),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def other_configs(dev, budget_s: float):
+    """One warm-up + one timed full pass (device-resident, CUDA events) of each
+    other BASELINE config, each checked against its oracle digest.  Configs are
+    skipped once the block has used `budget_s` seconds of wall time."""
+    import hashlib
+
+    import torch
+
+    import paper_2009_00083_b200 as P
+    from paper_2009_00083_b200 import synthetic as S
+    hp = os.path.join(ROOT, "tests", "golden", "full_hashes.json")
+    digests = json.load(open(hp)) if os.path.exists(hp) else {}
+    out = {}
+    t_start = time.time()
+    for c in (1, 2, 4, 5):
+        if time.time() - t_start > budget_s:
+            out[S.CONFIGS[c].name] = {"skipped": "time budget of the configs block used up"}
+            continue
+        C = S.CONFIGS[c]
+        f = S.make_field(c, 0).ravel()
+        mesh = P.build_grid_triangulation(C.dims)
+        fd = torch.from_numpy(f).to(dev)
+        F = P.compute_order_field(P.ScalarField(mesh, fd))
+        mn, mx = P.extrema(mesh, F)
+        pm, pn = S.select_preserved(F.rank32.cpu().numpy(), mx.cpu().numpy(), mn.cpu().numpy(),
+                                    C.n_keep_max, C.n_keep_min)
+        pm_d, pn_d = torch.from_numpy(pm).to(dev), torch.from_numpy(pn).to(dev)
+        g = torch.empty_like(fd)
+        G = torch.empty(mesh.n, dtype=torch.int32, device=dev)
+        opt = P.SimplifyOptions(collectTiming=True)
+        P.simplify_raw(mesh, fd, pm_d, pn_d, None, opt, g, G)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _, _, rep = P.simplify_raw(mesh, fd, pm_d, pn_d, None, opt, g, G)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        r = P.engine._report(rep)
+        d = digests.get(str(c), {})
+        out[C.name] = {
+            "n": mesh.n, "ms_per_pass": ms, "value": mesh.n / (ms * 1e-3), "unit": UNIT,
+            "preserve": [int(pm.size), int(pn.size)], "outer": r.outerIterations, "maxNI": r.maxNI,
+            "largest_region": r.largestRegion,
+            "phases_ms": {k: round(v, 3) for k, v in r.phase_ms.items()},
+            "G_matches_oracle": hashlib.sha256(G.cpu().numpy().tobytes()).hexdigest() == d.get("G_sha"),
+            "g_matches_oracle": hashlib.sha256(g.cpu().numpy().tobytes()).hexdigest() == d.get("g_sha"),
+            "oracle_cpu_s": (d.get("oracle_seconds") or {}).get("simplify"),
+        }
+        del fd, F, g, G
+        torch.cuda.empty_cache()
+    return out
 
 
 def large_field_kernels(dev, hbm):
@@ -208,11 +286,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-nz", type=int, default=32, help="z-planes in the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-large", action="store_true", help="skip the 512^3 kernel roofline block")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other-configs block")
+    ap.add_argument("--configs-budget", type=float, default=240.0,
+                    help="wall seconds after which the other-configs block stops starting configs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rendezvous on 127.0.0.1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29517"),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return reference_arm(args)
 
@@ -370,29 +456,32 @@ def main():
     if rank == 0 and world == 1 and not args.no_large:
         kernels_large = large_field_kernels(dev, hbm)
 
-    # ---- CPU baseline (rank 0, N = 1) ---------------------------------------
+    # ---- other BASELINE configs (rank 0, N = 1) -------------------------------
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = other_configs(dev, args.configs_budget)
+
+    # ---- CPU baseline (rank 0, N = 1): the same full pass on the host --------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        dims_s, fr, pms, pns = cpu_sample(f3d, cfg, args.cpu_nz)
+        dims_s, fr, pms, pns = cpu_workload(f3d, cfg)
         threads = os.cpu_count() or 1
         dt = run_oracle(dims_s, fr, pms, pns, threads)
         cpu = {"value": fr.size / dt, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": (f"first {args.cpu_nz} z-planes of the same field ({fr.size} voxels), "
-                          f"preserve {pms.size} max / {pns.size} min, one full pass, {dt:.1f} s; "
-                          f"OpenMP in classify/localize, discover/sort/realize sequential")}
+               "cpu_model": cpu_model(),
+               "sample": (f"the full workload ({cfg.name}, {fr.size} voxels, preserve {pms.size} max / "
+                          f"{pns.size} min), one full pass, {dt:.1f} s; OpenMP in classify/localize, "
+                          f"discover/sort/realize sequential as in the reference")}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} full LTS pass", "grid": list(cfg.dims), "n": n,
-                       "seed": args.seed, "preserve": [int(pm.size), int(pn.size)],
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "flushed between steps (256 MiB write, outside the per-step events)"},
+            "config": workload_config(cfg, args, n, (pm.size, pn.size), world),
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
             "kernels_large": kernels_large,
-            "phases_ms": phases, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "phases_ms": phases, "cpu_baseline": cpu, "clocks": clk.summary(), "configs": configs,
             "report": {"ok": report.ok, "outer": report.outerIterations,
                        "passes": [p.__dict__ for p in report.passes]},
             "step_ms": step_ms,

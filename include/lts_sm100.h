@@ -62,7 +62,14 @@ typedef struct {
   int32_t max_iterations;           /* SPEC.md:303 maxIterations (default 100)  */
   int32_t restore_interior_extrema; /* SPEC.md:302 (default 1)                  */
   int32_t collect_timing;           /* record CUDA-event phase times            */
-  int32_t reserved[5];
+  int32_t reserved0;
+  /* SPEC.md:306-309 per-region N_I: when non-NULL (device int32), every
+   * pass appends the N_I of each of its regions (region order of that pass,
+   * passes in execution order) while fewer than region_ni_capacity entries
+   * are written; lts_report_t.region_ni_count gives the total.               */
+  int32_t *region_ni_out;
+  int64_t region_ni_capacity;
+  int32_t reserved[4];
 } lts_options_t;
 
 typedef struct {
@@ -85,6 +92,7 @@ typedef struct {
   int32_t restored;          /* restored preserved extrema                     */
   int32_t n_passes;
   int64_t extra_max, lost_max, extra_min, lost_min; /* final verify counts     */
+  int64_t region_ni_count;   /* per-region N_I entries produced (all passes)   */
   lts_pass_report_t passes[LTS_MAX_REPORT_PASSES];
   double phase_ms[LTS_NUM_PHASES];
 } lts_report_t;
@@ -116,6 +124,19 @@ int lts_workspace_size(int ndim, const int64_t *dims, size_t *bytes);
 int lts_order_field(const float *f, int ndim, const int64_t *dims, int32_t *rank,
                     int32_t *inverse, void *ws, size_t ws_bytes, void *stream);
 
+/* ScalarField finiteness (reference order.py:35-36): LTS_E_FIELD_NONFINITE
+ * if f (device float32, n) holds a NaN or +-inf, else LTS_OK.  Synchronous. */
+int lts_check_field(const float *f, int64_t n, void *stream);
+
+/* Literal numeric realization: replaces realize_numeric / realize_sweep
+ * (order.py:102-116, _kernels.py:84-99) in float64.  g (device float64, n)
+ * holds f on entry and is lowered in place along the descending order of
+ * `inverse` (device int32, n): a vertex violating the order under (value, id)
+ * tie-breaking takes g[prev] - zeta, or nextafter(g[prev], -inf) when that
+ * does not decrease.  The sweep is sequential by definition; it runs on one
+ * CTA that stages the gathered values through shared memory. */
+int lts_realize_numeric(double *g, const int32_t *inverse, int64_t n, double zeta, void *stream);
+
 /* Classification: replaces classify_all / classify_grid (critical.py:95-112,
  * _kernels.py:128-156).  rank: device int32 n.  flags (device uint8 n, may be
  * NULL): bit0 minimum (lower==0), bit1 maximum (upper==0).  lower/upper
@@ -145,7 +166,8 @@ int lts_remove_pass(int kind, const int32_t *rank, const int32_t *inverse, const
  * added).  order (device int32 n) may be NULL, else it is
  * used as F instead of sorting f.  Outputs g (device float32 n) and G (device
  * int32 n, the final order's ranks).  rep/opt are host structs (opt may be
- * NULL for defaults). */
+ * NULL for defaults).  f and g may both be NULL when order is given
+ * (remove_extrema: orders only, no numeric realization). */
 int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *pres_max,
                  int64_t n_max, const int64_t *pres_min, int64_t n_min, const int32_t *order,
                  float *g, int32_t *G, lts_report_t *rep, const lts_options_t *opt, void *ws,

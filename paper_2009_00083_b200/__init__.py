@@ -9,7 +9,7 @@ from .errors import (ConstraintNotExtremum, FieldError, LocalizeError, LTSNative
                      NoSaddleError, VerifyError)
 from .triangulation import Triangulation, build_grid_triangulation, grid_link_tables, link_adjacency
 from .order import (OrderField, ScalarField, ZetaMode, ZetaPolicy, compute_order_field,
-                    order_from_ranks)
+                    order_from_ranks, realize_numeric)
 from .critical import (CriticalSet, Criticality, Kind, classify_all, classify_vertex,
                        extract_critical_points, extrema)
 from .engine import (ConstraintSet, PassRegions, SimplifyOptions, SimplifyReport, discover_regions,
@@ -21,7 +21,7 @@ __all__ = [
     "ConstraintNotExtremum", "FieldError", "LocalizeError", "LTSNativeError", "MeshError",
     "NoSaddleError", "VerifyError", "Triangulation", "build_grid_triangulation", "grid_link_tables",
     "link_adjacency", "OrderField", "ScalarField", "ZetaMode", "ZetaPolicy", "compute_order_field",
-    "order_from_ranks", "CriticalSet", "Criticality", "Kind", "classify_all", "classify_vertex",
+    "order_from_ranks", "realize_numeric", "CriticalSet", "Criticality", "Kind", "classify_all", "classify_vertex",
     "extract_critical_points", "extrema", "ConstraintSet", "PassRegions", "SimplifyOptions",
     "SimplifyReport", "discover_regions", "remove_extrema", "remove_pass", "simplify_field",
     "simplify_raw", "verify_constraints", "PersistencePairs", "compute_extremum_saddle_pairs",

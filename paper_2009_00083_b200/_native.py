@@ -34,7 +34,9 @@ PH_FLOOD_LAUNCHES, PH_FLOOD_SLOTS = 10, 11  # counts reported in phase_ms slots
 
 class lts_options_t(ctypes.Structure):
     _fields_ = [("max_iterations", ctypes.c_int32), ("restore_interior_extrema", ctypes.c_int32),
-                ("collect_timing", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("collect_timing", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("region_ni_out", ctypes.c_void_p), ("region_ni_capacity", ctypes.c_int64),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 class lts_pass_report_t(ctypes.Structure):
@@ -50,6 +52,7 @@ class lts_report_t(ctypes.Structure):
                 ("restored", ctypes.c_int32), ("n_passes", ctypes.c_int32),
                 ("extra_max", ctypes.c_int64), ("lost_max", ctypes.c_int64),
                 ("extra_min", ctypes.c_int64), ("lost_min", ctypes.c_int64),
+                ("region_ni_count", ctypes.c_int64),
                 ("passes", lts_pass_report_t * MAX_REPORT_PASSES),
                 ("phase_ms", ctypes.c_double * NUM_PHASES)]
 
@@ -63,7 +66,7 @@ class lts_regions_view_t(ctypes.Structure):
 
 EXPORTS = ["lts_version", "lts_last_error", "lts_workspace_size", "lts_order_field", "lts_classify",
            "lts_remove_pass", "lts_simplify", "lts_kernel_launches", "lts_debug_big_stats", "lts_bench_kernels",
-           "lts_extremum_pairs"]
+           "lts_extremum_pairs", "lts_check_field", "lts_realize_numeric"]
 
 _lib = None
 
@@ -94,6 +97,8 @@ def load():
                                ctypes.POINTER(lts_options_t), P, ctypes.c_size_t, P]
     L.lts_debug_big_stats.argtypes = [I, P, I]
     L.lts_bench_kernels.argtypes = [P, I, P, I, P, P, ctypes.c_size_t, P]
+    L.lts_check_field.argtypes = [P, I64, P]
+    L.lts_realize_numeric.argtypes = [P, P, I64, ctypes.c_double, P]
     L.lts_extremum_pairs.argtypes = [P, P, I, P, I, ctypes.c_double, P, P, ctypes.POINTER(I64), P,
                                      ctypes.c_size_t, P]
     for name in EXPORTS:
@@ -111,8 +116,11 @@ def require_cuda():
         raise NativeError("no CUDA device visible: the LTS path runs only on the GPU (no CPU fallback)")
 
 
-def stream_ptr():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def stream_ptr(device=None):
+    """The current torch stream of `device` (default: the current device).
+    Callers pass the device their tensors live on and run the call under
+    ``torch.cuda.device(device)`` so the library works on that device."""
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 def ptr(t):

@@ -62,18 +62,22 @@ def _kind_from_counts(lower: int, upper: int) -> Kind:
 
 def classify_flags(mesh: Triangulation, order: OrderField) -> torch.Tensor:
     """uint8 per vertex: bit0 minimum, bit1 maximum (device stencil)."""
-    flags = torch.empty(mesh.n, dtype=torch.uint8, device=order.rank32.device)
-    N.check(N.load().lts_classify(N.ptr(order.rank32), mesh.dim, N.dims_arg(mesh.grid_dims),
-                                  N.ptr(flags), None, None, N.stream_ptr()))
+    dev = order.rank32.device
+    flags = torch.empty(mesh.n, dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        N.check(N.load().lts_classify(N.ptr(order.rank32), mesh.dim, N.dims_arg(mesh.grid_dims),
+                                      N.ptr(flags), None, None, N.stream_ptr(dev)))
     return flags
 
 
 def classify_all(mesh: Triangulation, order: OrderField):
     """Lower/upper link component counts for every vertex (critical.py:95-112)."""
-    lower = torch.empty(mesh.n, dtype=torch.int16, device=order.rank32.device)
-    upper = torch.empty(mesh.n, dtype=torch.int16, device=order.rank32.device)
-    N.check(N.load().lts_classify(N.ptr(order.rank32), mesh.dim, N.dims_arg(mesh.grid_dims),
-                                  None, N.ptr(lower), N.ptr(upper), N.stream_ptr()))
+    dev = order.rank32.device
+    lower = torch.empty(mesh.n, dtype=torch.int16, device=dev)
+    upper = torch.empty(mesh.n, dtype=torch.int16, device=dev)
+    with torch.cuda.device(dev):
+        N.check(N.load().lts_classify(N.ptr(order.rank32), mesh.dim, N.dims_arg(mesh.grid_dims),
+                                      None, N.ptr(lower), N.ptr(upper), N.stream_ptr(dev)))
     return lower, upper
 
 

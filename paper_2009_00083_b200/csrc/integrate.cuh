@@ -12,6 +12,8 @@
 // sum_j min(l, k_j-1) + #{j : top_j < top_r, l <= k_j-2} over the sibling
 // regions j sharing the saddle (k_j = size incl. saddle).
 #pragma once
+#include <math_constants.h>
+
 #include "lts_common.cuh"
 
 namespace lts {
@@ -183,6 +185,58 @@ __global__ void k_restore_shift(int *rank, int64_t n, int x, int kind, const int
     } else {
       if (r > rx && r <= ry) rank[v] = r - 1;
     }
+  }
+}
+
+// Literal realize_sweep (reference _kernels.py:84-99) in float64: walk the
+// order from the top; a vertex that violates it under (value, id)
+// tie-breaking takes g[prev] - zeta (nextafter(g[prev], -inf) when that does
+// not decrease).  Inherently sequential: one CTA, the values of a chunk of
+// RZ_C positions gathered in parallel into shared memory, the chain run by
+// thread 0 over the chunk, the results scattered back in parallel.
+constexpr int RZ_T = 256, RZ_C = 2048;
+
+__global__ void __launch_bounds__(RZ_T) k_realize_sweep(double *g, const int *__restrict__ inverse, int64_t n,
+                                                        double zeta) {
+  __shared__ double s_val[RZ_C];
+  __shared__ int s_id[RZ_C];
+  __shared__ double s_prev_val;
+  __shared__ int s_prev;
+  if (threadIdx.x == 0) {
+    s_prev = inverse[n - 1];
+    s_prev_val = g[s_prev];
+  }
+  // positions n-2 .. 0 in chunks, top chunk first
+  for (int64_t hi = n - 2; hi >= 0; hi -= RZ_C) {
+    const int64_t lo = hi - RZ_C + 1 > 0 ? hi - RZ_C + 1 : 0;
+    const int cnt = (int)(hi - lo + 1);
+    for (int j = threadIdx.x; j < cnt; j += RZ_T) {  // j = 0 is position hi
+      const int v = inverse[hi - j];
+      s_id[j] = v;
+      s_val[j] = g[v];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int prev = s_prev;
+      double pv = s_prev_val;
+      for (int j = 0; j < cnt; j++) {
+        const int v = s_id[j];
+        double x = s_val[j];
+        if (x > pv || (x == pv && v > prev)) {
+          double nv = pv - zeta;
+          if (nv >= pv) nv = nextafter(pv, -CUDART_INF);
+          x = nv;
+          s_val[j] = x;
+        }
+        prev = v;
+        pv = x;
+      }
+      s_prev = prev;
+      s_prev_val = pv;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += RZ_T) g[s_id[j]] = s_val[j];
+    __syncthreads();
   }
 }
 

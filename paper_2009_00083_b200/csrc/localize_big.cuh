@@ -77,7 +77,8 @@ __device__ __forceinline__ int big_locate(const BigArgs &Bg, int i) {
 enum { BST_T = 0, BST_ACTIVE, BST_FIN, BST_STATUS, BST_BAD, BST_DIFF, BST_W = 8 };
 
 // optional per-region instrumentation (lts_debug_big_stats): big-queue slot i
-// records [k, steps, candidates, committed, flood cycles, -, -, n_iters,
+// records [k, frontier steps, candidates, committed, flood cycles, global-rule
+// steps, global-rule commits, n_iters,
 // gather, probe, cut, commit cycles, steps with j <= 8, j <= 32,
 // sum ceil(j/32), unpreempted steps, sum ceil(j/64)]
 constexpr int DBG_MAX = 256, DBG_W = 24;
@@ -89,6 +90,7 @@ struct BigSmem {
   int wsum[BIG_NW];
   int wmax[BIG_NW];
   int cut, hi_chunk, nw, nw4;
+  int ghi_chunk, gblock;  // global rule: highest possibly unextracted chunk, blocking key
   uint32_t *leaf;   // frontier bit set over keys
   uint32_t *seen;   // bit set over keys
   __align__(16) uint32_t bits[BIG_SMEM_WORDS];
@@ -134,22 +136,122 @@ __device__ __forceinline__ int big_scan_excl(int x, int *wsum, int &total) {
   return pre + inc - x;
 }
 
+// Top-BIG_B set bits of a key-space bit set, descending, one per thread.
+// word4(b) returns the four words b..b+3 (zero past the key range); hi_chunk
+// (shared) is an upper bound of the highest non-empty chunk and is lowered to
+// the highest chunk found non-empty.  A chunk of leaf words (thread 0 owns the
+// highest BIG_WPT words) is popcounted and scanned once; then candidate slot i
+// binary-searches the per-thread prefix for the owner of its key and selects
+// the bit, so every thread does the same small amount of work however the
+// keys cluster.  Returns the candidate count (block-uniform); key = -1 for
+// threads without a candidate.
+template <class W4>
+__device__ __forceinline__ int big_gather(BigSmem &S, int &hi_chunk, W4 word4, int &key) {
+  const int tid = threadIdx.x;
+  int nc = 0;
+  key = -1;
+  const int hi = hi_chunk;
+  int top_found = -1;
+  for (int ch = hi; ch >= 0 && nc < BIG_B; ch--) {
+    const int base = ch * BIG_CHUNK + (BIG_T - 1 - tid) * BIG_WPT;
+    const uint4 w = word4(base);
+    const int cnt = __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
+    int tot;
+    const int r = big_scan_excl(cnt, S.wsum, tot);
+    S.pref[tid] = r;
+    __syncthreads();
+    const int want = tid - nc;
+    if (want >= 0 && want < tot) {
+      int lo = 0, up = BIG_T - 1;  // owner: the last thread with pref <= want
+#pragma unroll
+      for (int it = 0; it < 16 && lo < up; it++) {
+        const int mid = (lo + up + 1) >> 1;
+        if (S.pref[mid] <= want) lo = mid;
+        else up = mid - 1;
+      }
+      int rem = want - S.pref[lo];
+      const int b0 = ch * BIG_CHUNK + (BIG_T - 1 - lo) * BIG_WPT;
+      const uint4 ow = word4(b0);
+      const uint32_t ws[4] = {ow.w, ow.z, ow.y, ow.x};  // highest word first
+#pragma unroll
+      for (int h = 0; h < 4; h++) {
+        const int c = __popc(ws[h]);
+        if (rem < c) {
+          const uint32_t x = ws[h];
+          const int need = rem + 1;  // need-th highest set bit of x
+          int bpos = 0;
+#pragma unroll
+          for (int sft = 16; sft >= 1; sft >>= 1)
+            if (__popc(x >> (bpos + sft)) >= need) bpos += sft;
+          key = ((b0 + 3 - h) << 5) + bpos;
+          break;
+        }
+        rem -= c;
+      }
+    }
+    if (tot > 0 && top_found < 0) top_found = ch;
+    nc = min(BIG_B, nc + tot);
+  }
+  __syncthreads();  // every thread has read hi_chunk
+  if (tid == 0) hi_chunk = top_found;  // chunks above it are empty
+  return nc;
+}
+
+__device__ __forceinline__ bool big_bit(const uint32_t *b, int x) { return (b[x >> 5] >> (x & 31)) & 1u; }
+
 template <int K>
-__device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, int *cout, long long *dbg) {
+__device__ __forceinline__ void big_row(const BigRegion &G, int key, int (&q)[K]) {
+  const int2 *row = reinterpret_cast<const int2 *>(G.krow + (size_t)key * K);
+#pragma unroll
+  for (int h = 0; h < K / 2; h++) {
+    const int2 v = row[h];
+    q[2 * h] = v.x;
+    q[2 * h + 1] = v.y;
+  }
+}
+
+// One exact priority flood of a large region (the e-th extraction gets label
+// k-1-e for descending floods, e for ascending ones).  Each iteration commits
+// an exact prefix of the extraction order by one of two rules:
+//  (g) global rule: let x_1 > x_2 > ... be the unextracted keys.  x_i is the
+//      i-th next extraction iff x_1..x_i are each in the frontier, or have a
+//      higher neighbour (which is then an earlier x_j), or an extracted
+//      neighbour: the frontier max is then always the largest unextracted
+//      key.  So the longest prefix of the top-B unextracted keys whose members
+//      pass that local test is committed at once.  Floods after the first
+//      (where the order is already nearly monotone) commit most of a region
+//      this way.  The first failing key is an unreached local maximum; the
+//      rule is skipped until that vertex enters the frontier.
+//  (f) frontier rule: with f1 > f2 > ... the frontier and new_i the unseen
+//      neighbours exposed by f_i, f1..fj are the next j extractions iff
+//      max key(new_1 u ... u new_i) < key(f_{i+1}) for every i < j.
+// Keys are a permutation of [0, k] minus one unused key (the region's local
+// order with the +-BIG sentinels of the first flood mapped to k and 0), so
+// the frontier ("leaf") and the seen set are bit sets over key space;
+// extracted = seen and not leaf.
+template <int K>
+__device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, int *cout, int unused_key,
+                          long long *dbg) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = G.k;
   uint32_t *const leaf = S.leaf;
   uint32_t *const seen = S.seen;
   const int nw = S.nw4;
+  const int nwv = S.nw;                       // words holding keys 0..k
+  const uint32_t lastmask = ((k + 1) & 31) ? ((1u << ((k + 1) & 31)) - 1u) : 0xffffffffu;
   for (int i = tid; i < nw; i += BIG_T) {
     leaf[i] = 0u;
     seen[i] = 0u;
   }
   if (tid == 0) {
     S.hi_chunk = -1;
+    S.ghi_chunk = k >> BIG_CHUNK_SHIFT;
+    S.gblock = -1;
     S.cut = 0x7fffffff;
   }
   __syncthreads();
+  // the one key no slot maps to counts as extracted
+  if (tid == 0) seen[unused_key >> 5] |= 1u << (unused_key & 31);
   // sources: the saddle (desc) or every admissible boundary minimum (asc)
   int mine = 0;
   if (!asc) {
@@ -179,86 +281,85 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     __syncthreads();
     return;
   }
+  const auto leaf4 = [&](int b) -> uint4 {
+    return b < nw ? *reinterpret_cast<const uint4 *>(leaf + b) : make_uint4(0u, 0u, 0u, 0u);
+  };
+  const auto unext4 = [&](int b) -> uint4 {  // unextracted = not seen, or in the frontier
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int i = b + j;
+      uint32_t x = i < nwv ? (~seen[i] | leaf[i]) : 0u;
+      if (i == nwv - 1) x &= lastmask;
+      w[j] = x;
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  };
   int e = 0;
-  long long tq = 0, tn, tg = 0, tp = 0, tc = 0, tm = 0, nst = 0, ncand = 0;
-  if (dbg && tid == 0) tq = clock64();
-#define BIG_TICK(acc)      \
-  if (dbg && tid == 0) {   \
-    tn = clock64();        \
-    acc += tn - tq;        \
-    tq = tn;               \
-  }
-  for (;;) {
-    // (a) candidates = the top B keys of F, descending, one per thread: a
-    // chunk of leaf words (thread 0 owns the highest BIG_WPT words) is
-    // popcounted and scanned once; then candidate slot i binary-searches the
-    // per-thread prefix for the owner of its key and selects the bit, so every
-    // thread does the same small amount of work however the keys cluster
-    int nc = 0, key = -1;
-    {
-      const int hi = S.hi_chunk;
-      int top_found = -1;
-      for (int ch = hi; ch >= 0 && nc < BIG_B; ch--) {
-        const int base = ch * BIG_CHUNK + (BIG_T - 1 - tid) * BIG_WPT;
-        uint4 w = make_uint4(0u, 0u, 0u, 0u);
-        if (base < S.nw4) w = *reinterpret_cast<const uint4 *>(leaf + base);
-        const int cnt = __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
-        int tot;
-        const int r = big_scan_excl(cnt, S.wsum, tot);
-        S.pref[tid] = r;
-        __syncthreads();
-        const int want = tid - nc;
-        if (want >= 0 && want < tot) {
-          int lo = 0, up = BIG_T - 1;  // owner: the last thread with pref <= want
+  long long nst = 0, ncand = 0, ngs = 0, ngc = 0;
+  while (e < k) {
+    int key, q[K];
+    // ---- (g) global rule ---------------------------------------------------
+    int j = 0;
+    const int gb = S.gblock;
+    if (gb < 0 || big_bit(seen, gb)) {
+      const int ng = big_gather(S, S.ghi_chunk, unext4, key);
+      const bool isc = tid < ng;
+      int cand_p = 0;
+      if (isc) {
+        cand_p = G.inv[key];
+        big_row<K>(G, key, q);
+        bool ok = big_bit(leaf, key);
 #pragma unroll
-          for (int it = 0; it < 16 && lo < up; it++) {
-            const int mid = (lo + up + 1) >> 1;
-            if (S.pref[mid] <= want) lo = mid;
-            else up = mid - 1;
-          }
-          int rem = want - S.pref[lo];
-          const int b0 = ch * BIG_CHUNK + (BIG_T - 1 - lo) * BIG_WPT;
-          const uint4 ow = *reinterpret_cast<const uint4 *>(leaf + b0);
-          const uint32_t ws[4] = {ow.w, ow.z, ow.y, ow.x};  // highest word first
-          int u = 3;
+        for (int kk = 0; kk < K; kk++) {
+          const int x = q[kk];
+          if (x > key) ok = true;                                          // a higher neighbour
+          else if (x >= 0 && big_bit(seen, x) && !big_bit(leaf, x)) ok = true;  // an extracted one
+          if (x < 0 || big_bit(seen, x)) q[kk] = -1;                      // keep the exposures
+        }
+        const unsigned bad = __ballot_sync(__activemask(), !ok);
+        if (bad && lane == __ffs(bad) - 1) atomicMin(&S.cut, tid);
+      }
+      __syncthreads();
+      j = min(S.cut, ng);
+      if (j < ng && tid == j) S.gblock = key;  // first failing key: an unreached local maximum
+      if (j == ng && tid == 0) S.gblock = -1;
+      if (j > 0) {
+        int mch = -1;
+        if (tid < j) {
+          cout[cand_p] = asc ? (e + tid) : (k - 1 - (e + tid));
+          atomicOr(seen + (key >> 5), 1u << (key & 31));
 #pragma unroll
-          for (int h = 0; h < 4; h++) {
-            const int c = __popc(ws[h]);
-            if (rem < c) {
-              u = 3 - h;
-              const uint32_t x = ws[h];
-              const int need = rem + 1;  // need-th highest set bit of x
-              int bpos = 0;
-#pragma unroll
-              for (int sft = 16; sft >= 1; sft >>= 1)
-                if (__popc(x >> (bpos + sft)) >= need) bpos += sft;
-              key = ((b0 + u) << 5) + bpos;
-              break;
+          for (int kk = 0; kk < K; kk++) {
+            const int x = q[kk];
+            if (x >= 0) {
+              atomicOr(seen + (x >> 5), 1u << (x & 31));
+              atomicOr(leaf + (x >> 5), 1u << (x & 31));
+              mch = max(mch, x >> BIG_CHUNK_SHIFT);
             }
-            rem -= c;
           }
         }
-        if (tot > 0 && top_found < 0) top_found = ch;
-        nc = min(BIG_B, nc + tot);
+        mch = __reduce_max_sync(0xffffffffu, mch);
+        if (lane == 0 && mch >= 0) atomicMax(&S.hi_chunk, mch);
+        __syncthreads();
+        if (tid < j) atomicAnd(leaf + (key >> 5), ~(1u << (key & 31)));
+        e += j;
+        ngs++;
+        ngc += j;
       }
-      if (tid == 0) S.hi_chunk = top_found;  // chunks above it are empty
+      __syncthreads();
+      if (tid == 0) S.cut = 0x7fffffff;
+      __syncthreads();
+      if (j > 0) continue;
     }
-    BIG_TICK(tg)
+    // ---- (f) frontier rule ---------------------------------------------------
+    const int nc = big_gather(S, S.hi_chunk, leaf4, key);
     if (nc == 0) break;
-    // (b) probes: thread i owns candidate i; its row of neighbour keys and
-    // its local index come from L2 in one round trip
     const bool isc = tid < nc;
-    int q[K];
     int cand_p = 0;
     if (isc) {
       cand_p = G.inv[key];
-      const int2 *row = reinterpret_cast<const int2 *>(G.krow + (size_t)key * K);
-#pragma unroll
-      for (int h = 0; h < K / 2; h++) {
-        const int2 v = row[h];
-        q[2 * h] = v.x;
-        q[2 * h + 1] = v.y;
-      }
+      big_row<K>(G, key, q);
     } else {
 #pragma unroll
       for (int kk = 0; kk < K; kk++) q[kk] = -1;
@@ -267,12 +368,11 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
       const int x = q[kk];
-      if (x >= 0 && !((seen[x >> 5] >> (x & 31)) & 1u)) nm = max(nm, x);
+      if (x >= 0 && !big_bit(seen, x)) nm = max(nm, x);
       else q[kk] = -1;
     }
-    BIG_TICK(tp)
-    // (c) first preemption: exclusive prefix max of the exposures in
-    // candidate order against the candidate's own key
+    // first preemption: exclusive prefix max of the exposures in candidate
+    // order against the candidate's own key
     {
       int inc = nm;
 #pragma unroll
@@ -292,10 +392,9 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
       if (lane == 0 && bal) atomicMin(&S.cut, warp * 32 + __ffs(bal) - 1);
       __syncthreads();
     }
-    const int j = min(S.cut, nc);
-    BIG_TICK(tc)
-    // (d) commit the prefix: labels, leave F; its exposures join F (setting a
-    // bit twice is harmless, so the updates need no return value)
+    j = min(S.cut, nc);
+    // commit the prefix: labels, leave F; its exposures join F (setting a bit
+    // twice is harmless, so the updates need no return value)
     int mch = -1;
     if (tid < j) {
       cout[cand_p] = asc ? (e + tid) : (k - 1 - (e + tid));
@@ -324,17 +423,14 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     }
     __syncthreads();
     if (tid == 0) S.cut = 0x7fffffff;
-    BIG_TICK(tm)
+    __syncthreads();
   }
-#undef BIG_TICK
   if (dbg && tid == 0) {
     dbg[1] += nst;
     dbg[2] += ncand;
     dbg[3] += e;
-    dbg[8] += tg;
-    dbg[9] += tp;
-    dbg[10] += tc;
-    dbg[11] += tm;
+    dbg[5] += ngs;
+    dbg[6] += ngc;
   }
 }
 
@@ -536,7 +632,10 @@ __global__ void __launch_bounds__(BIG_T) k_big_flood(LocArgs A, BigArgs Bg) {
   if (dbg && tid == 0) dbg[0] = k;
   if (tid == 0) atomicAdd(Bg.work, (unsigned long long)k);
   const long long c0 = clock64();
-  big_flood<K>(S, G, t & 1, big_buf(A, t) + lo, big_buf(A, t + 1) + lo, dbg);
+  // the key no slot maps to: v0's index in the first flood (its slot maps to
+  // key 0 and the saddle's to k), k in every later one
+  const int unused_key = t == 0 ? Bg.v0[qi] : k;
+  big_flood<K>(S, G, t & 1, big_buf(A, t) + lo, big_buf(A, t + 1) + lo, unused_key, dbg);
   if (dbg && tid == 0) dbg[4] += clock64() - c0;
 }
 

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -132,30 +133,58 @@ static void build_lut(int ndim, std::vector<uint8_t> &lut) {
   }
 }
 
-static bool g_tables_ready = false;
+// ---------------------------------------------------------------------------
+// Per-device state.  __constant__ / __device__ symbols, streams, events and
+// function attributes belong to one device, so everything the library caches
+// is kept per device (indexed by cudaGetDevice), and every C ABI entry point
+// holds g_mu for its duration (one call at a time per process; the calls are
+// synchronous on their stream anyway).
+// ---------------------------------------------------------------------------
+constexpr int LTS_MAX_DEV = 64;
+struct DevState {
+  bool tables_ready = false;
+  int off_ndim = 0;
+  int *h_scal = nullptr;  // pinned scalar readback slots
+  std::vector<cudaEvent_t> events;
+  size_t ev_next = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool big_attr = false;
+  int coop_blocks = 0;
+};
+static DevState g_dev[LTS_MAX_DEV];
+static DevState *g_cur = &g_dev[0];
+static std::recursive_mutex g_mu;
+#define LTS_LOCK std::lock_guard<std::recursive_mutex> lts_lock_(g_mu)
+
+static int select_device() {
+  int d = 0;
+  LTS_CUDA(cudaGetDevice(&d));
+  if (d < 0 || d >= LTS_MAX_DEV) return lts_set_error(LTS_E_INVALID, "device index out of range");
+  g_cur = &g_dev[d];
+  return 0;
+}
 
 static int init_tables() {
-  if (g_tables_ready) return 0;
+  if (g_cur->tables_ready) return 0;
   std::vector<uint8_t> l2, l3;
   build_lut(2, l2);
   build_lut(3, l3);
   LTS_CUDA(cudaMemcpyToSymbol(d_lut2, l2.data(), l2.size()));
   LTS_CUDA(cudaMemcpyToSymbol(d_lut3, l3.data(), l3.size()));
-  g_tables_ready = true;
+  g_cur->tables_ready = true;
   return 0;
 }
 
-static int g_off_ndim = 0;
-
 static int set_offsets(int ndim, cudaStream_t s) {
-  if (g_off_ndim == ndim) return 0;
+  if (g_cur->off_ndim == ndim) return 0;
   int8_t off[3][kMaxK] = {};
   int K = ndim == 2 ? 6 : 14;
   for (int k = 0; k < K; k++)
     for (int a = 0; a < 3; a++) off[a][k] = ndim == 2 ? H_OFF2[k][a] : H_OFF3[k][a];
   LTS_CUDA(cudaMemcpyToSymbolAsync(c_off, off, sizeof(off), 0, cudaMemcpyHostToDevice, s));
   LTS_CUDA(cudaStreamSynchronize(s));
-  g_off_ndim = ndim;
+  g_cur->off_ndim = ndim;
   return 0;
 }
 
@@ -287,17 +316,14 @@ struct Ctx {
   int64_t flood_launches = 0, flood_slots = 0;
 };
 
-static int *g_h_scal = nullptr;
-static std::vector<cudaEvent_t> g_events;
-static size_t g_ev_next = 0;
-
 static cudaEvent_t next_event() {
-  if (g_ev_next >= g_events.size()) {
+  DevState &d = *g_cur;
+  if (d.ev_next >= d.events.size()) {
     cudaEvent_t e;
     cudaEventCreate(&e);
-    g_events.push_back(e);
+    d.events.push_back(e);
   }
-  return g_events[g_ev_next++];
+  return d.events[d.ev_next++];
 }
 
 struct Phase {
@@ -350,6 +376,7 @@ static int setup(Ctx &c, int ndim, const int64_t *dims, void *ws, size_t ws_byte
   c.g.n = n;
   c.n = n;
   c.s = (cudaStream_t)stream;
+  LTS_TRY(select_device());
   int64_t need = carve(&c.w, nullptr, ndim, n);
   if (ws != nullptr) {
     if ((size_t)need > ws_bytes) return lts_set_error(LTS_E_WORKSPACE, "workspace too small");
@@ -359,10 +386,10 @@ static int setup(Ctx &c, int ndim, const int64_t *dims, void *ws, size_t ws_byte
   LTS_TRY(set_offsets(ndim, c.s));
   c.lut = lut_ptr(ndim);
   if (!c.lut) return lts_set_error(LTS_E_CUDA, "cudaGetSymbolAddress failed for the link LUT");
-  if (!g_h_scal) LTS_CUDA(cudaHostAlloc((void **)&g_h_scal, sizeof(int) * SC_N, cudaHostAllocDefault));
-  c.h_scal = g_h_scal;
+  if (!g_cur->h_scal) LTS_CUDA(cudaHostAlloc((void **)&g_cur->h_scal, sizeof(int) * SC_N, cudaHostAllocDefault));
+  c.h_scal = g_cur->h_scal;
   c.timing = false;
-  g_ev_next = 0;
+  g_cur->ev_next = 0;
   return 0;
 }
 
@@ -393,17 +420,16 @@ __global__ void k_count_big(const int *rsize, int R, int th, int *out) {
   }
 }
 
-static cudaStream_t g_side = nullptr, g_bigs = nullptr;
-static cudaEvent_t g_fork = nullptr, g_join = nullptr;
-static bool g_big_attr = false;
+static cudaStream_t g_bigs = nullptr;  // stream of the current call's large-region floods
 
 static int big_stream_fork(cudaStream_t s) {
-  if (!g_side) {
-    LTS_CUDA(cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking));
-    LTS_CUDA(cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming));
-    LTS_CUDA(cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming));
+  DevState &d = *g_cur;
+  if (!d.side) {
+    LTS_CUDA(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
+    LTS_CUDA(cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming));
+    LTS_CUDA(cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming));
   }
-  if (!g_big_attr) {
+  if (!d.big_attr) {
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
     // leave the rest of the unified L1/shared array to L1: the floods re-read
@@ -411,22 +437,22 @@ static int big_stream_fork(cudaStream_t s) {
     int carve = (int)((sizeof(BigSmem) * 100 + 227 * 1024 - 1) / (228 * 1024)) + 1;
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<3>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    g_big_attr = true;
+    d.big_attr = true;
   }
   // LTS_BIG_SERIAL (diagnostic): run the large-region floods on the main
   // stream, alone on the GPU
   static const bool serial = getenv("LTS_BIG_SERIAL") != nullptr;
-  g_bigs = serial ? s : g_side;
+  g_bigs = serial ? s : d.side;
   if (serial) return 0;
-  LTS_CUDA(cudaEventRecord(g_fork, s));
-  LTS_CUDA(cudaStreamWaitEvent(g_bigs, g_fork, 0));
+  LTS_CUDA(cudaEventRecord(d.fork, s));
+  LTS_CUDA(cudaStreamWaitEvent(g_bigs, d.fork, 0));
   return 0;
 }
 
 static int big_stream_join(cudaStream_t s) {
   if (g_bigs == s) return 0;
-  LTS_CUDA(cudaEventRecord(g_join, g_bigs));
-  LTS_CUDA(cudaStreamWaitEvent(s, g_join, 0));
+  LTS_CUDA(cudaEventRecord(g_cur->join, g_bigs));
+  LTS_CUDA(cudaStreamWaitEvent(s, g_cur->join, 0));
   return 0;
 }
 
@@ -551,7 +577,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     // Boruvka rounds: tau(m) = bottleneck to preserved maxima, all rounds in
     // one cooperative launch (grid barriers between phases); one readback
     {
-      static int coop_blocks = 0;
+      int &coop_blocks = g_cur->coop_blocks;
       if (!coop_blocks) {
         int dev = 0, nsm = 0, per = 0;
         cudaGetDevice(&dev);
@@ -725,6 +751,30 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     view->status = w.st;
     view->topseed = w.rtop;
   }
+  return 0;
+}
+
+// A caller-supplied order field F (simplify_field(order=F), remove_extrema,
+// lts_extremum_pairs): copied to rankA with its inverse in invA.  F must be a
+// bijection onto [0, n) (else LTS_E_INVALID) and f, when given, must be
+// finite (reference ScalarField, order.py:35-36; else LTS_E_FIELD_NONFINITE).
+static int install_order(Ctx &c, const float *f, const int32_t *order) {
+  WS &w = c.w;
+  const int64_t n = c.n;
+  cudaStream_t s = c.s;
+  LTS_CUDA(cudaMemcpyAsync(w.rankA, order, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  LTS_CUDA(cudaMemsetAsync(w.invA, 0xff, sizeof(int) * n, s));
+  LTS_CUDA(cudaMemsetAsync(w.scal + SC_TMP, 0, sizeof(int) * 2, s));
+  k_scatter_inverse_checked<<<NB(n), 256, 0, s>>>(w.rankA, w.invA, n, w.scal + SC_TMP);
+  g_launches++;
+  if (f) {
+    k_nonfinite<<<grid_blocks(n, 256, 148 * 8), 256, 0, s>>>(f, n, w.scal + SC_TMP + 1);
+    g_launches++;
+  }
+  LTS_KCHECK();
+  LTS_TRY(readback(c, SC_TMP, 2));
+  if (c.h_scal[SC_TMP + 1]) return lts_set_error(LTS_E_FIELD_NONFINITE, "scalar field contains NaN or infinite values");
+  if (c.h_scal[SC_TMP]) return lts_set_error(LTS_E_INVALID, "order is not a permutation of 0..n-1");
   return 0;
 }
 
@@ -918,6 +968,7 @@ static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, i
 int lts_extremum_pairs(const float *f, const int32_t *order, int ndim, const int64_t *dims, int kind, double epsilon,
                        int32_t *extrema_out, int32_t *saddle_out, int64_t *count_out, void *ws, size_t ws_bytes,
                        void *stream) {
+  LTS_LOCK;
   Ctx c;
   LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
   if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
@@ -925,9 +976,7 @@ int lts_extremum_pairs(const float *f, const int32_t *order, int ndim, const int
   if (!(epsilon >= 0)) return lts_set_error(LTS_E_INVALID, "epsilon must be >= 0");
   WS &w = c.w;
   if (order) {
-    LTS_CUDA(cudaMemcpyAsync(w.rankA, order, sizeof(int) * c.n, cudaMemcpyDeviceToDevice, c.s));
-    k_scatter_inverse<<<NB(c.n), 256, 0, c.s>>>(w.rankA, w.invA, c.n);
-    g_launches++;
+    LTS_TRY(install_order(c, f, order));
   } else {
     LTS_TRY(order_field_impl(c, f, w.rankA, w.invA));
   }
@@ -938,6 +987,7 @@ int lts_extremum_pairs(const float *f, const int32_t *order, int ndim, const int
 
 int lts_bench_kernels(const float *f, int ndim, const int64_t *dims, int reps, double *out_ms, void *ws,
                       size_t ws_bytes, void *stream) {
+  LTS_LOCK;
   Ctx c;
   LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
   if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
@@ -984,6 +1034,7 @@ int lts_bench_kernels(const float *f, int ndim, const int64_t *dims, int reps, d
 
 // diagnostics: enable/read the per-region counters of the CTA flood kernel
 int lts_debug_big_stats(int enable, int64_t *out, int nregions) {
+  LTS_LOCK;
   int on = enable ? 1 : 0;
   LTS_CUDA(cudaMemcpyToSymbol(d_dbg_on, &on, sizeof(int)));
   if (enable) {
@@ -1032,8 +1083,41 @@ static int order_field_impl(Ctx &c, const float *f, int32_t *rank, int32_t *inve
   return 0;
 }
 
+int lts_check_field(const float *f, int64_t n, void *stream) {
+  LTS_LOCK;
+  LTS_TRY(select_device());
+  if (n <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!g_cur->h_scal) LTS_CUDA(cudaHostAlloc((void **)&g_cur->h_scal, sizeof(int) * SC_N, cudaHostAllocDefault));
+  int *d = nullptr;
+  LTS_CUDA(cudaMallocAsync((void **)&d, sizeof(int), s));
+  LTS_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
+  k_nonfinite<<<grid_blocks(n, 256, 148 * 8), 256, 0, s>>>(f, n, d);
+  g_launches++;
+  LTS_KCHECK();
+  LTS_CUDA(cudaMemcpyAsync(g_cur->h_scal + SC_TMP, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LTS_CUDA(cudaFreeAsync(d, s));
+  LTS_CUDA(cudaStreamSynchronize(s));
+  if (g_cur->h_scal[SC_TMP]) return lts_set_error(LTS_E_FIELD_NONFINITE, "scalar field contains NaN or infinite values");
+  return 0;
+}
+
+int lts_realize_numeric(double *g, const int32_t *inverse, int64_t n, double zeta, void *stream) {
+  LTS_LOCK;
+  LTS_TRY(select_device());
+  if (!(zeta >= 0)) return lts_set_error(LTS_E_INVALID, "zeta must be >= 0");
+  if (n < 2) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_realize_sweep<<<1, RZ_T, 0, s>>>(g, inverse, n, zeta);
+  g_launches++;
+  LTS_KCHECK();
+  LTS_CUDA(cudaStreamSynchronize(s));
+  return 0;
+}
+
 int lts_order_field(const float *f, int ndim, const int64_t *dims, int32_t *rank, int32_t *inverse,
                     void *ws, size_t ws_bytes, void *stream) {
+  LTS_LOCK;
   Ctx c;
   LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
   if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
@@ -1042,6 +1126,7 @@ int lts_order_field(const float *f, int ndim, const int64_t *dims, int32_t *rank
 
 int lts_classify(const int32_t *rank, int ndim, const int64_t *dims, uint8_t *flags, int16_t *lower,
                  int16_t *upper, void *stream) {
+  LTS_LOCK;
   Ctx c;
   LTS_TRY(setup(c, ndim, dims, nullptr, 0, stream));
   if ((lower == nullptr) != (upper == nullptr)) return lts_set_error(LTS_E_INVALID, "lower and upper go together");
@@ -1054,6 +1139,7 @@ int lts_remove_pass(int kind, const int32_t *rank, const int32_t *inverse, const
                     const int64_t *dims, int32_t max_iterations, int32_t *new_rank, int32_t *new_inverse,
                     float *g, lts_pass_report_t *rep, lts_regions_view_t *view, void *ws, size_t ws_bytes,
                     void *stream) {
+  LTS_LOCK;
   Ctx c;
   LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
   if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
@@ -1065,9 +1151,12 @@ int lts_remove_pass(int kind, const int32_t *rank, const int32_t *inverse, const
 int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *pres_max, int64_t n_max,
                  const int64_t *pres_min, int64_t n_min, const int32_t *order, float *g, int32_t *G,
                  lts_report_t *rep, const lts_options_t *opt, void *ws, size_t ws_bytes, void *stream) {
+  LTS_LOCK;
   Ctx c;
   LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
   if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
+  if ((f == nullptr) != (g == nullptr)) return lts_set_error(LTS_E_INVALID, "f and g go together");
+  if (!f && !order) return lts_set_error(LTS_E_INVALID, "f is required unless an order field is given");
   lts_options_t o{};
   o.max_iterations = 100;
   o.restore_interior_extrema = 1;
@@ -1085,9 +1174,7 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
   }
   // A1/A2: order field F
   if (order) {
-    LTS_CUDA(cudaMemcpyAsync(w.rankA, order, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
-    k_scatter_inverse<<<NB(n), 256, 0, s>>>(w.rankA, w.invA, n);
-    g_launches++;
+    LTS_TRY(install_order(c, f, order));
   } else {
     LTS_TRY(order_field_impl(c, f, w.rankA, w.invA));
   }
@@ -1104,8 +1191,8 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
     launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, w.ptr, PTR_ASC, s);
   }
   k_check_pres<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, w.scal + SC_BADPRES);
-  k_copy_canon<<<NB(n), 256, 0, s>>>(f, g, n);
-  g_launches += 4;
+  if (g) k_copy_canon<<<NB(n), 256, 0, s>>>(f, g, n);
+  g_launches += g ? 4 : 3;
   LTS_KCHECK();
   LTS_TRY(readback(c, SC_BADPRES, 1));
   if (c.h_scal[SC_BADPRES]) return lts_set_error(LTS_E_CONSTRAINT_NOT_EXTREMUM, "a preserved vertex is not an extremum of the input order (ConstraintNotExtremum)");
@@ -1119,6 +1206,14 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
       LTS_TRY(run_pass(c, kind, cr, ci, w.pmark, o.max_iterations, nr, ni, g, &pr, nullptr,
                        it == 1 && kind == 0));
       if (R.n_passes < LTS_MAX_REPORT_PASSES) R.passes[R.n_passes++] = pr;
+      if (o.region_ni_out && pr.regions > 0) {  // per-region N_I
+        const int64_t room = o.region_ni_capacity - R.region_ni_count;
+        const int64_t cnt = std::min<int64_t>(room, pr.regions);
+        if (cnt > 0)
+          LTS_CUDA(cudaMemcpyAsync(o.region_ni_out + R.region_ni_count, w.nit, sizeof(int) * cnt,
+                                   cudaMemcpyDeviceToDevice, s));
+        R.region_ni_count += pr.regions;
+      }
       std::swap(cr, nr);
       std::swap(ci, ni);
     }

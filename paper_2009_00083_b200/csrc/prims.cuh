@@ -132,4 +132,28 @@ __global__ void k_scatter_inverse(const int *__restrict__ rank, int *inverse, in
     inverse[rank[v]] = (int)v;
 }
 
+// order_from_ranks with validation: inverse must be pre-filled with -1; a rank
+// outside [0, n) or a rank taken twice (so `rank` is not a bijection) sets *bad
+__global__ void k_scatter_inverse_checked(const int *__restrict__ rank, int *inverse, int64_t n, int *bad) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rank[v];
+    if (r < 0 || (int64_t)r >= n) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    if (atomicExch(inverse + r, (int)v) != -1) atomicOr(bad, 1);
+  }
+}
+
+// ScalarField finiteness (reference order.py:35-36) for callers that bring
+// their own order field: NaN or +-inf sets *bad
+__global__ void k_nonfinite(const float *__restrict__ f, int64_t n, int *bad) {
+  bool b = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b |= (__float_as_uint(f[i]) & 0x7f800000u) == 0x7f800000u;
+  if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 }  // namespace lts

@@ -48,8 +48,20 @@ __global__ void __launch_bounds__(256) k_hist(const uint32_t *__restrict__ keys,
   __syncthreads();
   bool bad = false;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t n4 = n / 4;
-  const uint4 *k4 = reinterpret_cast<const uint4 *>(keys);
+  // the caller's array may start at any 4-byte boundary (a view with a
+  // storage offset): the first `head` keys are read one by one, the rest as
+  // 16-byte vectors
+  const int64_t head = min(n, (int64_t)(((16u - ((uint32_t)(uintptr_t)keys & 15u)) & 15u) >> 2));
+  const int64_t n4 = (n - head) / 4;
+  const uint4 *k4 = reinterpret_cast<const uint4 *>(keys + head);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < head; i += stride) {
+    uint32_t x = keys[i];
+    if (FLOATKEY) {
+      if ((x & 0x7f800000u) == 0x7f800000u) bad = true;
+      x = float_key(x);
+    }
+    for (int p = 0; p < npasses; p++) atomicAdd(&sh[p][(x >> (8 * p)) & 255], 1u);
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     uint4 q = __ldg(k4 + i);
     uint32_t u[4] = {q.x, q.y, q.z, q.w};
@@ -63,7 +75,7 @@ __global__ void __launch_bounds__(256) k_hist(const uint32_t *__restrict__ keys,
       for (int p = 0; p < npasses; p++) atomicAdd(&sh[p][(x >> (8 * p)) & 255], 1u);
     }
   }
-  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (int64_t i = head + n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     uint32_t x = keys[i];
     if (FLOATKEY) {
       if ((x & 0x7f800000u) == 0x7f800000u) bad = true;

@@ -21,7 +21,7 @@ import torch
 from . import _native as N
 from .critical import classify_flags, extrema
 from .errors import ConstraintNotExtremum
-from .order import OrderField, ScalarField, ZetaPolicy, compute_order_field, _as_cuda
+from .order import OrderField, ScalarField, ZetaPolicy, ZetaMode, compute_order_field, realize_numeric, _as_cuda
 from .triangulation import Triangulation
 
 
@@ -35,14 +35,28 @@ class ConstraintSet:
 
 @dataclass
 class SimplifyOptions:
-    """SPEC SimplifyOptions.  threadCount has no meaning on
-    the device and is accepted for signature compatibility."""
+    """SPEC SimplifyOptions.
 
-    zeta: ZetaPolicy = field(default_factory=ZetaPolicy)
+    zeta: None (default) realises g by contract D1: per pass, every
+    flattened vertex takes its region saddle's value, so g only holds copies of
+    input values.  A ZetaPolicy instead applies SPEC's literal
+    ``g = realize_numeric(f, G, zeta)`` (float64 output, order.py:102-116).
+    threadCount: the reference's CPU thread count; the device path's result
+    does not depend on it, values < 0 are rejected."""
+
+    zeta: Optional[ZetaPolicy] = None
     restoreInteriorExtrema: bool = True
     maxIterations: int = 100
     threadCount: int = 0
     collectTiming: bool = False
+
+    def __post_init__(self):
+        if int(self.maxIterations) < 1:
+            raise ValueError("maxIterations must be >= 1 (SPEC.md:304)")
+        if int(self.threadCount) < 0:
+            raise ValueError("threadCount must be >= 0")
+        if self.zeta is not None and not isinstance(self.zeta, ZetaPolicy):
+            raise TypeError("zeta must be a ZetaPolicy or None")
 
 
 @dataclass
@@ -72,6 +86,7 @@ class SimplifyReport:
     largestRegion: int
     maxNI: int
     capped: int
+    regionNI: list = field(default_factory=list)  # per pass: int32 tensor of each region's N_I
     linf: Optional[float] = None
     phase_ms: dict = field(default_factory=dict)
     extra_max: int = 0
@@ -100,7 +115,7 @@ def _ids(x, device) -> torch.Tensor:
     return t.reshape(-1).contiguous()
 
 
-def _report(rep: "N.lts_report_t") -> SimplifyReport:
+def _report(rep: "N.lts_report_t", ni: Optional[torch.Tensor] = None) -> SimplifyReport:
     passes = []
     for i in range(rep.n_passes):
         p = rep.passes[i]
@@ -113,30 +128,49 @@ def _report(rep: "N.lts_report_t") -> SimplifyReport:
         passes=passes, regionCount=sum(p.regions for p in passes),
         largestRegion=max([p.largest for p in passes] + [0]),
         maxNI=max([p.n_iter_max for p in passes] + [0]), capped=sum(p.capped for p in passes),
+        regionNI=_split_ni(ni, passes, int(rep.region_ni_count)),
         phase_ms=ph, extra_max=int(rep.extra_max), lost_max=int(rep.lost_max),
         extra_min=int(rep.extra_min), lost_min=int(rep.lost_min))
 
 
-def simplify_raw(mesh: Triangulation, values: torch.Tensor, pres_max: torch.Tensor,
+def _split_ni(ni, passes, count):
+    if ni is None:
+        return []
+    out, off = [], 0
+    for p in passes:
+        out.append(ni[off:off + p.regions] if off + p.regions <= ni.numel() else None)
+        off += p.regions
+    return out
+
+
+def simplify_raw(mesh: Triangulation, values: Optional[torch.Tensor], pres_max: torch.Tensor,
                  pres_min: torch.Tensor, order: Optional[torch.Tensor] = None,
-                 options: Optional[SimplifyOptions] = None, g_out=None, G_out=None):
-    """Device-tensor entry point: values float32 (cuda), pres_* int64 (cuda).
-    Returns (g float32, G int32 ranks, lts_report_t).  No host copies."""
+                 options: Optional[SimplifyOptions] = None, g_out=None, G_out=None, ni_out=None):
+    """Device-tensor entry point: values float32 (cuda; None = orders only,
+    then `order` is required), pres_* int64 (cuda).  ni_out (optional int32
+    device tensor) receives the per-region N_I of every pass.
+    Returns (g float32 or None, G int32 ranks, lts_report_t).  No host copies."""
     options = options or SimplifyOptions()
-    dev = values.device
-    g = g_out if g_out is not None else torch.empty(mesh.n, dtype=torch.float32, device=dev)
+    dev = values.device if values is not None else order.device
+    g = None
+    if values is not None:
+        g = g_out if g_out is not None else torch.empty(mesh.n, dtype=torch.float32, device=dev)
     G = G_out if G_out is not None else torch.empty(mesh.n, dtype=torch.int32, device=dev)
     ws = N.workspace(mesh.grid_dims, dev)
     opt = N.lts_options_t()
     opt.max_iterations = int(options.maxIterations)
     opt.restore_interior_extrema = 1 if options.restoreInteriorExtrema else 0
     opt.collect_timing = 1 if options.collectTiming else 0
+    if ni_out is not None:
+        opt.region_ni_out = ni_out.data_ptr()
+        opt.region_ni_capacity = ni_out.numel()
     rep = N.lts_report_t()
-    rc = N.load().lts_simplify(N.ptr(values), mesh.dim, N.dims_arg(mesh.grid_dims), N.ptr(pres_max),
-                               pres_max.numel(), N.ptr(pres_min), pres_min.numel(),
-                               N.ptr(order) if order is not None else None, N.ptr(g), N.ptr(G),
-                               ctypes.byref(rep), ctypes.byref(opt), N.ptr(ws), ws.numel(),
-                               N.stream_ptr())
+    with torch.cuda.device(dev):
+        rc = N.load().lts_simplify(N.ptr(values), mesh.dim, N.dims_arg(mesh.grid_dims), N.ptr(pres_max),
+                                   pres_max.numel(), N.ptr(pres_min), pres_min.numel(),
+                                   N.ptr(order) if order is not None else None, N.ptr(g), N.ptr(G),
+                                   ctypes.byref(rep), ctypes.byref(opt), N.ptr(ws), ws.numel(),
+                                   N.stream_ptr(dev))
     N.check(rc)
     return g, G, rep
 
@@ -147,14 +181,22 @@ def simplify_field(mesh: Triangulation, f, constraints: ConstraintSet,
     Returns (g: ScalarField, G: OrderField, SimplifyReport)."""
     if not isinstance(f, ScalarField):
         f = ScalarField(mesh, f)
+    options = options or SimplifyOptions()
     dev = f.values.device
     pmax = _ids(constraints.preserveMaxima, dev)
     pmin = _ids(constraints.preserveMinima, dev)
+    ni = torch.empty(mesh.n, dtype=torch.int32, device=dev)
     g, G, rep = simplify_raw(mesh, f.values, pmax, pmin,
-                             order.rank32 if order is not None else None, options)
-    report = _report(rep)
+                             order.rank32 if order is not None else None, options, ni_out=ni)
+    report = _report(rep, ni)
+    Gf = OrderField(rank32=G)
+    if options.zeta is not None:
+        # SPEC.md:351 literal post-condition g = realize_numeric(f, G, zeta)
+        gf = realize_numeric(f, Gf, options.zeta)
+        report.linf = float((gf.values - f.values.to(torch.float64)).abs().max()) if mesh.n else 0.0
+        return gf, Gf, report
     report.linf = float((g - f.values).abs().max()) if mesh.n else 0.0
-    return ScalarField(mesh, g), OrderField(rank32=G), report
+    return ScalarField._wrap(mesh, g), Gf, report
 
 
 def remove_extrema(mesh: Triangulation, F: OrderField, discardMaxima, discardMinima,
@@ -170,9 +212,10 @@ def remove_extrema(mesh: Triangulation, F: OrderField, discardMaxima, discardMin
         raise ConstraintNotExtremum("a discard vertex is not a minimum of F")
     pmax = mx[~torch.isin(mx, dmax)]
     pmin = mn[~torch.isin(mn, dmin)]
-    dummy = torch.zeros(mesh.n, dtype=torch.float32, device=dev)
-    _, G, rep = simplify_raw(mesh, dummy, pmax.contiguous(), pmin.contiguous(), F.rank32, options)
-    return OrderField(rank32=G), _report(rep)
+    ni = torch.empty(mesh.n, dtype=torch.int32, device=dev)
+    _, G, rep = simplify_raw(mesh, None, pmax.contiguous(), pmin.contiguous(), F.rank32.contiguous(), options,
+                             ni_out=ni)
+    return OrderField(rank32=G), _report(rep, ni)
 
 
 @dataclass
@@ -221,11 +264,12 @@ def remove_pass(mesh: Triangulation, F: OrderField, preserve: ConstraintSet, kin
     ws = N.workspace(mesh.grid_dims, dev)
     rep = N.lts_pass_report_t()
     view = N.lts_regions_view_t()
-    N.check(N.load().lts_remove_pass(0 if kind == "max" else 1, N.ptr(F.rank32), N.ptr(inv), N.ptr(pmark),
-                                     mesh.dim, N.dims_arg(mesh.grid_dims), int(max_iterations),
-                                     N.ptr(nr), N.ptr(ni), None, ctypes.byref(rep),
-                                     ctypes.byref(view), N.ptr(ws), ws.numel(), N.stream_ptr()))
-    torch.cuda.current_stream().synchronize()
+    with torch.cuda.device(dev):
+        N.check(N.load().lts_remove_pass(0 if kind == "max" else 1, N.ptr(F.rank32), N.ptr(inv), N.ptr(pmark),
+                                         mesh.dim, N.dims_arg(mesh.grid_dims), int(max_iterations),
+                                         N.ptr(nr), N.ptr(ni), None, ctypes.byref(rep),
+                                         ctypes.byref(view), N.ptr(ws), ws.numel(), N.stream_ptr(dev)))
+        torch.cuda.current_stream(dev).synchronize()
     R, S = int(view.regions), int(view.slots)
     pr = PassReport(kind, rep.seeds, rep.regions, rep.claimed, rep.largest, rep.n_iter_max,
                     rep.capped, rep.shared_saddles, rep.maxima_edges, rep.boruvka_rounds,

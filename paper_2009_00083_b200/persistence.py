@@ -62,9 +62,10 @@ def compute_extremum_saddle_pairs(mesh: Triangulation, f, F: Optional[OrderField
     cnt = ctypes.c_int64(0)
     ws = N.workspace(mesh.grid_dims, dev)
     order = F.rank32 if F is not None else None
-    N.check(N.load().lts_extremum_pairs(N.ptr(vals), N.ptr(order), mesh.dim, N.dims_arg(mesh.grid_dims),
-                                        0 if polarity == "max" else 1, float(epsilon), N.ptr(ext), N.ptr(sad),
-                                        ctypes.byref(cnt), N.ptr(ws), ws.numel(), N.stream_ptr()))
+    with torch.cuda.device(dev):
+        N.check(N.load().lts_extremum_pairs(N.ptr(vals), N.ptr(order), mesh.dim, N.dims_arg(mesh.grid_dims),
+                                            0 if polarity == "max" else 1, float(epsilon), N.ptr(ext), N.ptr(sad),
+                                            ctypes.byref(cnt), N.ptr(ws), ws.numel(), N.stream_ptr(dev)))
     k = int(cnt.value)
     e = ext[:k].to(torch.int64)
     s = sad[:k].to(torch.int64)

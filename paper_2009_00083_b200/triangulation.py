@@ -102,6 +102,9 @@ class Triangulation:
         return int(self.neighbors(v).size)
 
 
+MAX_GRID_VERTICES = 1 << 27  # liblts_sm100.so's limit (512^3), same check as lts_sm100.cu setup()
+
+
 def build_grid_triangulation(dims, spacing: float = 1.0) -> Triangulation:
     """reference triangulation.py:128-169 (without the CSR arrays)."""
     dims = tuple(int(d) for d in dims)
@@ -110,8 +113,9 @@ def build_grid_triangulation(dims, spacing: float = 1.0) -> Triangulation:
     if any(d < 2 for d in dims):
         raise MeshError(f"every grid axis needs at least 2 vertices, got {dims}")
     n = int(np.prod(dims))
-    if n >= 2 ** 30:
-        raise MeshError(f"grid too large for int32 device ranks (n={n})")
+    if n > MAX_GRID_VERTICES:
+        raise MeshError(f"grid too large for the device path (n={n} > 2^27): the classification "
+                        "kernel packs rank << 4 | stencil index into 32 bits")
     return Triangulation(dim=len(dims), n=n, grid_dims=dims, spacing=spacing)
 
 

@@ -116,3 +116,45 @@ def test_select_preserved_top_k():
     mn = np.array([1, 4, 6])
     pm, pn = S.select_preserved(rank, mx, mn, 2, 1)
     assert pm.tolist() == [3, 7] and pn.tolist() == [1]
+
+
+def test_grid_size_limit_matches_library():
+    """One n limit on both sides of the boundary (MeshError / LTS_E_BAD_DIMS):
+    the device path packs rank << 4 | stencil index into 32 bits."""
+    import paper_2009_00083_b200 as P
+    P.build_grid_triangulation((512, 512, 512))  # 2^27: allowed
+    with pytest.raises(P.MeshError):
+        P.build_grid_triangulation((513, 512, 512))
+    assert P.triangulation.MAX_GRID_VERTICES == 1 << 27
+
+
+def test_simplify_options_validation():
+    import paper_2009_00083_b200 as P
+    assert P.SimplifyOptions().zeta is None  # contract D1 by default
+    with pytest.raises(ValueError):
+        P.SimplifyOptions(maxIterations=0)
+    with pytest.raises(ValueError):
+        P.SimplifyOptions(threadCount=-1)
+    with pytest.raises(TypeError):
+        P.SimplifyOptions(zeta=1e-12)
+    # the reference's ZetaPolicy default (order.py:77)
+    assert P.ZetaPolicy().mode is P.ZetaMode.RELATIVE_EPSILON
+    assert P.ZetaPolicy().step(2.0) == 2e-12
+    assert P.ZetaPolicy(P.ZetaMode.ULP_DECREMENT).step(2.0) == 0.0
+
+
+def test_float64_exactness_check_host_side():
+    from paper_2009_00083_b200.order import _to_f32_exact
+    from paper_2009_00083_b200 import FieldError
+    a = np.array([0.5, 1.25, -3.0, 2.0 ** 100], np.float64)
+    assert _to_f32_exact(a).dtype == np.float32
+    with pytest.raises(FieldError):
+        _to_f32_exact(np.array([0.1], np.float64))  # not a float32
+    assert _to_f32_exact(np.array([0.1], np.float32)).dtype == np.float32
+
+
+def test_bench_cli_refuses_nothing_on_cpu_parse():
+    """bench.py parses --gpus N and re-launches itself under torchrun when it
+    is not already a torchrun rank (checked by reading its argument handling)."""
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert "torch.distributed.run" in src and "--nproc-per-node" in src
