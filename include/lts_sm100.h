@@ -120,6 +120,7 @@ int lts_workspace_size(int ndim, const int64_t *dims, size_t *bytes);
 /* Order field F: replaces compute_order_field (order.py:86-91) and the
  * finiteness check of ScalarField (order.py:30-36).  Stable by (value, id);
  * -0.0 == +0.0.  f, rank, inverse: device, n.  inverse may be NULL.
+ * ndim 1 with dims = {n}: the vertices of an explicit mesh.
  * Returns LTS_E_FIELD_NONFINITE on NaN/inf (synchronises stream). */
 int lts_order_field(const float *f, int ndim, const int64_t *dims, int32_t *rank,
                     int32_t *inverse, void *ws, size_t ws_bytes, void *stream);
@@ -184,6 +185,38 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
 int lts_extremum_pairs(const float *f, const int32_t *order, int ndim, const int64_t *dims, int kind,
                        double epsilon, int32_t *extrema_out, int32_t *saddle_out, int64_t *count_out, void *ws,
                        size_t ws_bytes, void *stream);
+
+/* ---- explicit triangle meshes ---------------------------
+ * The reference's explicit 2-manifold meshes (build_explicit_triangulation,
+ * triangulation.py:172-250) reach its kernels as a symmetric CSR adjacency
+ * indptr[n+1] / indices[nnz] plus per-vertex link edges (link_ptr[n+1],
+ * link_a / link_b: the two other vertices of every triangle of the vertex).
+ * The device path takes the same arrays (device int32).  Vertex degrees must
+ * be <= 16 (LTS_E_BAD_DIMS otherwise).  lts_order_field covers explicit meshes
+ * with ndim = 1, dims = {n}. */
+
+/* Workspace bytes for an explicit mesh of n vertices. */
+int lts_workspace_size_csr(int64_t n, size_t *bytes);
+
+/* classify_all on an explicit mesh: replaces classify_explicit
+ * (_kernels.py:159-187).  flags / lower / upper as lts_classify; the link
+ * arrays are needed only for the counts (may be NULL with lower/upper NULL). */
+int lts_classify_csr(const int32_t *rank, int64_t n, const int32_t *indptr, const int32_t *indices,
+                     const int32_t *link_ptr, const int32_t *link_a, const int32_t *link_b, uint8_t *flags,
+                     int16_t *lower, int16_t *upper, void *stream);
+
+/* lts_remove_pass on an explicit mesh (discover_sweep / localize_regions over
+ * the CSR, _kernels.py:194-303, 578-591). */
+int lts_remove_pass_csr(int kind, const int32_t *rank, const int32_t *inverse, const uint8_t *pmark, int64_t n,
+                        const int32_t *indptr, const int32_t *indices, int32_t max_iterations, int32_t *new_rank,
+                        int32_t *new_inverse, float *g, lts_pass_report_t *rep, lts_regions_view_t *view, void *ws,
+                        size_t ws_bytes, void *stream);
+
+/* lts_simplify on an explicit mesh (SPEC.md:348-356 over any triangulation). */
+int lts_simplify_csr(const float *f, int64_t n, const int32_t *indptr, const int32_t *indices,
+                     const int64_t *pres_max, int64_t n_max, const int64_t *pres_min, int64_t n_min,
+                     const int32_t *order, float *g, int32_t *G, lts_report_t *rep, const lts_options_t *opt,
+                     void *ws, size_t ws_bytes, void *stream);
 
 /* Roofline micro-benchmarks (diagnostics): L2 flushed before each rep, CUDA
  * events around the kernel(s) only.  out_ms (host, 4): [0] order-field sort,

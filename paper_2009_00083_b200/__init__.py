@@ -6,8 +6,10 @@ order.py / critical.py / triangulation.py types, backed by hand-written CUDA in
 liblts_sm100.so.  See DESIGN.md.
 """
 from .errors import (ConstraintNotExtremum, FieldError, LocalizeError, LTSNativeError, MeshError,
-                     NoSaddleError, VerifyError)
-from .triangulation import Triangulation, build_grid_triangulation, grid_link_tables, link_adjacency
+                     NonManifoldEdge, NonTriangleFace, NoSaddleError, VerifyError)
+from .triangulation import (Triangulation, build_explicit_triangulation, build_grid_triangulation,
+                            grid_link_tables, link_adjacency, load_off, make_icosahedron, make_octahedron,
+                            make_torus, write_off)
 from .order import (OrderField, ScalarField, ZetaMode, ZetaPolicy, compute_order_field,
                     order_from_ranks, realize_numeric)
 from .critical import (CriticalSet, Criticality, Kind, classify_all, classify_vertex,
@@ -19,8 +21,9 @@ from .persistence import (PersistencePairs, compute_extremum_saddle_pairs, persi
 
 __all__ = [
     "ConstraintNotExtremum", "FieldError", "LocalizeError", "LTSNativeError", "MeshError",
-    "NoSaddleError", "VerifyError", "Triangulation", "build_grid_triangulation", "grid_link_tables",
-    "link_adjacency", "OrderField", "ScalarField", "ZetaMode", "ZetaPolicy", "compute_order_field",
+    "NonManifoldEdge", "NonTriangleFace", "NoSaddleError", "VerifyError", "Triangulation",
+    "build_explicit_triangulation", "build_grid_triangulation", "grid_link_tables", "link_adjacency",
+    "load_off", "write_off", "make_octahedron", "make_icosahedron", "make_torus", "OrderField", "ScalarField", "ZetaMode", "ZetaPolicy", "compute_order_field",
     "order_from_ranks", "realize_numeric", "CriticalSet", "Criticality", "Kind", "classify_all", "classify_vertex",
     "extract_critical_points", "extrema", "ConstraintSet", "PassRegions", "SimplifyOptions",
     "SimplifyReport", "discover_regions", "remove_extrema", "remove_pass", "simplify_field",

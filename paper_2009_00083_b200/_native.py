@@ -66,7 +66,8 @@ class lts_regions_view_t(ctypes.Structure):
 
 EXPORTS = ["lts_version", "lts_last_error", "lts_workspace_size", "lts_order_field", "lts_classify",
            "lts_remove_pass", "lts_simplify", "lts_kernel_launches", "lts_debug_big_stats", "lts_bench_kernels",
-           "lts_extremum_pairs", "lts_check_field", "lts_realize_numeric"]
+           "lts_extremum_pairs", "lts_check_field", "lts_realize_numeric", "lts_workspace_size_csr",
+           "lts_classify_csr", "lts_remove_pass_csr", "lts_simplify_csr"]
 
 _lib = None
 
@@ -98,6 +99,13 @@ def load():
     L.lts_debug_big_stats.argtypes = [I, P, I]
     L.lts_bench_kernels.argtypes = [P, I, P, I, P, P, ctypes.c_size_t, P]
     L.lts_check_field.argtypes = [P, I64, P]
+    L.lts_workspace_size_csr.argtypes = [I64, ctypes.POINTER(ctypes.c_size_t)]
+    L.lts_classify_csr.argtypes = [P, I64, P, P, P, P, P, P, P, P, P]
+    L.lts_remove_pass_csr.argtypes = [I, P, P, P, I64, P, P, ctypes.c_int32, P, P, P,
+                                      ctypes.POINTER(lts_pass_report_t), ctypes.POINTER(lts_regions_view_t),
+                                      P, ctypes.c_size_t, P]
+    L.lts_simplify_csr.argtypes = [P, I64, P, P, P, I64, P, I64, P, P, P, ctypes.POINTER(lts_report_t),
+                                   ctypes.POINTER(lts_options_t), P, ctypes.c_size_t, P]
     L.lts_realize_numeric.argtypes = [P, P, I64, ctypes.c_double, P]
     L.lts_extremum_pairs.argtypes = [P, P, I, P, I, ctypes.c_double, P, P, ctypes.POINTER(I64), P,
                                      ctypes.c_size_t, P]
@@ -135,15 +143,19 @@ def dims_arg(dims):
 _ws_cache: dict = {}
 
 
-def workspace(dims, device=None):
-    """Cached device workspace for a grid shape (caller-owned memory)."""
-    dims = tuple(int(d) for d in dims)
+def workspace(dims, device=None, explicit_n=None):
+    """Cached device workspace for a grid shape, or for an explicit mesh of
+    explicit_n vertices (caller-owned memory)."""
+    dims = tuple(int(d) for d in dims) if explicit_n is None else ("csr", int(explicit_n))
     device = torch.device(device or "cuda")
     key = (dims, str(device))
     ws = _ws_cache.get(key)
     if ws is None:
         nbytes = ctypes.c_size_t(0)
-        check(load().lts_workspace_size(len(dims), dims_arg(dims), ctypes.byref(nbytes)))
+        if explicit_n is None:
+            check(load().lts_workspace_size(len(dims), dims_arg(dims), ctypes.byref(nbytes)))
+        else:
+            check(load().lts_workspace_size_csr(int(explicit_n), ctypes.byref(nbytes)))
         ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=device)
         _ws_cache.clear()  # keep one workspace alive at a time
         _ws_cache[key] = ws

@@ -60,13 +60,27 @@ def _kind_from_counts(lower: int, upper: int) -> Kind:
     return Kind.SADDLE
 
 
+def _classify(mesh: Triangulation, order: OrderField, flags, lower, upper):
+    """lts_classify on grids (classify_grid, _kernels.py:128-156) or
+    lts_classify_csr on explicit meshes (classify_explicit, :159-187)."""
+    dev = order.rank32.device
+    L = N.load()
+    with torch.cuda.device(dev):
+        if mesh.is_grid:
+            N.check(L.lts_classify(N.ptr(order.rank32), mesh.dim, N.dims_arg(mesh.grid_dims),
+                                   N.ptr(flags), N.ptr(lower), N.ptr(upper), N.stream_ptr(dev)))
+        else:
+            d = mesh.device_arrays(dev)
+            N.check(L.lts_classify_csr(N.ptr(order.rank32), mesh.n, N.ptr(d["indptr"]), N.ptr(d["indices"]),
+                                       N.ptr(d["link_ptr"]), N.ptr(d["link_a"]), N.ptr(d["link_b"]),
+                                       N.ptr(flags), N.ptr(lower), N.ptr(upper), N.stream_ptr(dev)))
+
+
 def classify_flags(mesh: Triangulation, order: OrderField) -> torch.Tensor:
     """uint8 per vertex: bit0 minimum, bit1 maximum (device stencil)."""
     dev = order.rank32.device
     flags = torch.empty(mesh.n, dtype=torch.uint8, device=dev)
-    with torch.cuda.device(dev):
-        N.check(N.load().lts_classify(N.ptr(order.rank32), mesh.dim, N.dims_arg(mesh.grid_dims),
-                                      N.ptr(flags), None, None, N.stream_ptr(dev)))
+    _classify(mesh, order, flags, None, None)
     return flags
 
 
@@ -75,9 +89,7 @@ def classify_all(mesh: Triangulation, order: OrderField):
     dev = order.rank32.device
     lower = torch.empty(mesh.n, dtype=torch.int16, device=dev)
     upper = torch.empty(mesh.n, dtype=torch.int16, device=dev)
-    with torch.cuda.device(dev):
-        N.check(N.load().lts_classify(N.ptr(order.rank32), mesh.dim, N.dims_arg(mesh.grid_dims),
-                                      None, N.ptr(lower), N.ptr(upper), N.stream_ptr(dev)))
+    _classify(mesh, order, None, lower, upper)
     return lower, upper
 
 

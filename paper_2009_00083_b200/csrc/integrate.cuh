@@ -156,14 +156,13 @@ __global__ void k_lost(const uint8_t *__restrict__ flags, const uint8_t *__restr
 // neighbour; scal[0] = rx, scal[1] = ry, scal[2] = apply
 template <int NDIM>
 __global__ void k_restore_target(Grid g, const int *__restrict__ rank, int x, int kind, int *scal) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int cx, cy, cz;
-  coords(g, x, cx, cy, cz);
+  const Nb<NDIM> nb(g, x);
   int rx = rank[x];
   int ry = kind == 0 ? 0x7fffffff : -1;
   for (int k = 0; k < K; k++) {
-    int u = nbr_at(g, cx, cy, cz, k);
+    int u = nb(g, k);
     if (u < 0) continue;
     int ru = rank[u];
     if (kind == 0 ? ru < ry : ru > ry) ry = ru;

@@ -98,7 +98,7 @@ __device__ __forceinline__ int member(const LocArgs &A, int u, int rid, int s) {
 template <int NDIM>
 __device__ void flood(const LocArgs &A, bool asc, int rid, int s, int k, const int *verts,
                       const int *cin, int *cout, uint8_t *sfl, unsigned long long *heap) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   const int lane = threadIdx.x & 31;
   for (int p = lane; p < k; p += 32) sfl[p] &= (uint8_t)~SF_INHEAP;
   __syncwarp();
@@ -139,9 +139,8 @@ __device__ void flood(const LocArgs &A, bool asc, int rid, int s, int k, const i
     int v = verts[p];
     int q = -1, key = 0;
     if (lane < K) {
-      int x, y, z;
-      coords(A.g, v, x, y, z);
-      int u = nbr_at(A.g, x, y, z, lane);
+      const Nb<NDIM> nb(A.g, v);
+      int u = nb(A.g, lane);
       q = member(A, u, rid, s);
       if (q >= 0) {
         if (sfl[q] & SF_INHEAP) {
@@ -170,18 +169,17 @@ __device__ void flood(const LocArgs &A, bool asc, int rid, int s, int k, const i
 template <int NDIM>
 __device__ bool check_minima(const LocArgs &A, int rid, int s, int k, const int *verts,
                              const int *cur, uint8_t *sfl) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   const int lane = threadIdx.x & 31;
   bool bad = false;
   for (int p = 1 + lane; p < k; p += 32) {
     int v = verts[p];
-    int x, y, z;
-    coords(A.g, v, x, y, z);
+    const Nb<NDIM> nb(A.g, v);
     int c = cur[p];
     bool mn = true;
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
-      int q = member(A, nbr_at(A.g, x, y, z, kk), rid, s);
+      int q = member(A, nb(A.g, kk), rid, s);
       if (q >= 0 && cur[q] < c) {
         mn = false;
         break;
@@ -200,18 +198,17 @@ __device__ bool check_minima(const LocArgs &A, int rid, int s, int k, const int 
 template <int NDIM>
 __device__ bool check_maxima(const LocArgs &A, int rid, int s, int k, const int *verts,
                              const int *cur) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   const int lane = threadIdx.x & 31;
   bool bad = false;
   for (int p = 1 + lane; p < k; p += 32) {
     int v = verts[p];
-    int x, y, z;
-    coords(A.g, v, x, y, z);
+    const Nb<NDIM> nb(A.g, v);
     int c = cur[p];
     bool mx = true;
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
-      int q = member(A, nbr_at(A.g, x, y, z, kk), rid, s);
+      int q = member(A, nb(A.g, kk), rid, s);
       if (q >= 0 && cur[q] > c) {
         mx = false;
         break;
@@ -232,7 +229,7 @@ __device__ __forceinline__ bool states_equal(const int *a, const int *b, int k) 
 
 template <int NDIM>
 __global__ void __launch_bounds__(32 * LOC_WARPS) k_localize(LocArgs A) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   __shared__ unsigned long long s_heap[LOC_WARPS][LOC_SMEM_HEAP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int n = (int)A.g.n;
@@ -255,11 +252,10 @@ __global__ void __launch_bounds__(32 * LOC_WARPS) k_localize(LocArgs A) {
     for (int p = lane; p < k; p += 32) {
       bool out = false;
       if (p >= 1) {
-        int x, y, z;
-        coords(A.g, verts[p], x, y, z);
+        const Nb<NDIM> nb(A.g, verts[p]);
 #pragma unroll
         for (int kk = 0; kk < K; kk++) {
-          int u = nbr_at(A.g, x, y, z, kk);
+          int u = nb(A.g, kk);
           if (u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) {
             out = true;
             break;

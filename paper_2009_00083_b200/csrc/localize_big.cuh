@@ -78,9 +78,10 @@ enum { BST_T = 0, BST_ACTIVE, BST_FIN, BST_STATUS, BST_BAD, BST_DIFF, BST_W = 8 
 
 // optional per-region instrumentation (lts_debug_big_stats): big-queue slot i
 // records [k, frontier steps, candidates, committed, flood cycles, global-rule
-// steps, global-rule commits, n_iters,
-// gather, probe, cut, commit cycles, steps with j <= 8, j <= 32,
-// sum ceil(j/32), unpreempted steps, sum ceil(j/64)]
+// steps, global-rule commits, n_iters, frontier-rule gather, probe, cut,
+// commit cycles, steps with j <= 8, j <= 32, sum ceil(j/32), unpreempted
+// steps, warp-mode steps, global-rule cycles, global-rule attempts, warp-mode
+// cycles, warp-step gather / probe / cut+commit cycles]
 constexpr int DBG_MAX = 256, DBG_W = 24;
 __device__ long long d_dbg[DBG_MAX * DBG_W];
 __device__ int d_dbg_on;
@@ -89,10 +90,15 @@ struct BigSmem {
   int pref[BIG_T];
   int wsum[BIG_NW];
   int wmax[BIG_NW];
-  int cut, hi_chunk, nw, nw4;
+  int cutbuf[2], hi_chunk, nw, nw4;  // cut: first failing candidate (double-buffered per step)
   int ghi_chunk, gblock;  // global rule: highest possibly unextracted chunk, blocking key
+  int hi_sw, nsw4;        // frontier summary: highest possibly non-empty summary word, words
+  int hw;                 // highest possibly non-empty leaf word (warp mode)
+  int keep_sum;           // the summary is maintained (large regions only)
+  int wmode, ew;          // warp mode on; extraction count handed back by warp 0
   uint32_t *leaf;   // frontier bit set over keys
   uint32_t *seen;   // bit set over keys
+  uint32_t *sum;    // frontier summary: bit w set iff leaf word w is non-zero
   __align__(16) uint32_t bits[BIG_SMEM_WORDS];
 };
 
@@ -146,13 +152,13 @@ __device__ __forceinline__ int big_scan_excl(int x, int *wsum, int &total) {
 // keys cluster.  Returns the candidate count (block-uniform); key = -1 for
 // threads without a candidate.
 template <class W4>
-__device__ __forceinline__ int big_gather(BigSmem &S, int &hi_chunk, W4 word4, int &key) {
+__device__ __forceinline__ int big_gather(BigSmem &S, int &hi_chunk, W4 word4, int &key, int *iters = nullptr) {
   const int tid = threadIdx.x;
   int nc = 0;
   key = -1;
   const int hi = hi_chunk;
-  int top_found = -1;
-  for (int ch = hi; ch >= 0 && nc < BIG_B; ch--) {
+  int top_found = -1, nit = 0;
+  for (int ch = hi; ch >= 0 && nc < BIG_B; ch--, nit++) {
     const int base = ch * BIG_CHUNK + (BIG_T - 1 - tid) * BIG_WPT;
     const uint4 w = word4(base);
     const int cnt = __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
@@ -192,12 +198,37 @@ __device__ __forceinline__ int big_gather(BigSmem &S, int &hi_chunk, W4 word4, i
     if (tot > 0 && top_found < 0) top_found = ch;
     nc = min(BIG_B, nc + tot);
   }
-  __syncthreads();  // every thread has read hi_chunk
-  if (tid == 0) hi_chunk = top_found;  // chunks above it are empty
+  // chunks above top_found are empty (when the loop ran no chunk, hi < 0 and
+  // the value written is unchanged, so no barrier is needed against readers)
+  if (tid == 0) hi_chunk = top_found;
+  if (iters) *iters = nit;
   return nc;
 }
 
 __device__ __forceinline__ bool big_bit(const uint32_t *b, int x) { return (b[x >> 5] >> (x & 31)) & 1u; }
+
+// rem-th highest set bit of x (rem < popc(x))
+__device__ __forceinline__ int big_nth_high(uint32_t x, int rem) {
+  const int need = rem + 1;
+  int bpos = 0;
+#pragma unroll
+  for (int sft = 16; sft >= 1; sft >>= 1)
+    if (__popc(x >> (bpos + sft)) >= need) bpos += sft;
+  return bpos;
+}
+
+// ---- frontier summary -----------------------------------------------------
+// sum bit w is set whenever leaf word w gains a key and cleared lazily by the
+// warp gather when it finds the word empty.  A stale set bit only costs a
+// look; a cleared bit over a non-empty word cannot happen because bits are
+// cleared only by the gathering warp while no other warp commits.
+#ifndef LTS_BIG_SUM_MIN_WORDS
+#define LTS_BIG_SUM_MIN_WORDS 4096  // regions with fewer leaf words scan without a summary
+#endif
+__device__ __forceinline__ void big_front_add(BigSmem &S, int x, bool ks) {
+  atomicOr(S.leaf + (x >> 5), 1u << (x & 31));
+  if (ks) atomicOr(S.sum + (x >> 10), 1u << ((x >> 5) & 31));
+}
 
 template <int K>
 __device__ __forceinline__ void big_row(const BigRegion &G, int key, int (&q)[K]) {
@@ -209,6 +240,109 @@ __device__ __forceinline__ void big_row(const BigRegion &G, int key, int (&q)[K]
     q[2 * h + 1] = v.y;
   }
 }
+
+// largest lane u with v_u <= t for a lane-ascending (non-decreasing) v
+__device__ __forceinline__ int warp_owner(int v, int t) {
+  int lo = 0;
+#pragma unroll
+  for (int sft = 16; sft >= 1; sft >>= 1)
+    if (__shfl_sync(0xffffffffu, v, lo + sft) <= t) lo += sft;
+  return lo;
+}
+
+__device__ __forceinline__ int warp_incl_sum(int x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// Highest non-empty leaf word <= w0 (or -1), for the single warp: the
+// summary words are read 32 at a time from w0's downward; a set summary bit
+// whose leaf word turns out empty (stale: the summary is only ever set on
+// insert) is cleared by the caller, which then asks again.
+__device__ __forceinline__ int big_warp_next_word(BigSmem &S, int w0) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t *const sum = S.sum;
+  for (int s0 = w0 >> 5; s0 >= 0; s0 -= 32) {
+    const int sw = s0 - lane;
+    uint32_t m = sw >= 0 ? sum[sw] : 0u;
+    if (sw == (w0 >> 5)) m &= (w0 & 31) == 31 ? 0xffffffffu : ((2u << (w0 & 31)) - 1u);
+    const unsigned nz = __ballot_sync(0xffffffffu, m != 0u);
+    if (nz) {
+      const int l = __ffs(nz) - 1;
+      const uint32_t ml = __shfl_sync(0xffffffffu, m, l);
+      return (s0 - l) * 32 + 31 - __clz(ml);
+    }
+  }
+  return -1;
+}
+
+// Frontier keys for the single-warp step, descending, lane i gets the i-th
+// (-1 past the count): every frontier key of the 32 leaf words below the
+// highest non-empty one (at most 32 of them).  Any exact prefix of the
+// frontier order is a valid candidate list, so a sparse window simply yields
+// fewer candidates -- and rough floods commit only a few keys per step
+// anyway.  Lowers hw to the top non-empty word.
+__device__ int big_warp_gather(BigSmem &S, int &key) {
+  const int lane = threadIdx.x & 31;
+  volatile uint32_t *const leaf = S.leaf;
+  key = -1;
+  int hw = S.hw;
+  int nc = 0;
+  while (hw >= 0) {
+    const int w = hw - lane;
+    const uint32_t lw = w >= 0 ? leaf[w] : 0u;
+    const unsigned nz = __ballot_sync(0xffffffffu, lw != 0u);
+    if (nz == 0u && !S.keep_sum) {  // small region: no summary, step down a window
+      hw -= 32;
+      continue;
+    }
+    if (nz == 0u) {
+      // an empty window: clear its (stale) summary bits, then jump to the
+      // next non-empty word the summary knows of
+      if (lane == 0) {
+        const int lo = max(hw - 31, 0);
+        for (int sw = hw >> 5; sw >= (lo >> 5); sw--) {
+          const int a = max(lo, sw * 32) - sw * 32, b = min(hw, sw * 32 + 31) - sw * 32;
+          const uint32_t mask = (b == 31 ? 0xffffffffu : ((2u << b) - 1u)) & ~((1u << a) - 1u);
+          atomicAnd(S.sum + sw, ~mask);
+        }
+      }
+      __syncwarp();
+      hw = big_warp_next_word(S, hw - 32);
+      continue;
+    }
+    const int top = __ffs(nz) - 1;  // lanes run from the highest word down
+    const int c = __popc(lw);
+    const int inc = warp_incl_sum(c);
+    const int tot = __shfl_sync(0xffffffffu, inc, 31);
+    const int ex = inc - c;
+    const int o = warp_owner(ex, lane);
+    const uint32_t lwo = __shfl_sync(0xffffffffu, lw, o);
+    const int eo = __shfl_sync(0xffffffffu, ex, o);
+    if (lane < tot) key = ((hw - o) << 5) + big_nth_high(lwo, lane - eo);
+    nc = min(32, tot);
+    hw -= top;
+    break;
+  }
+  if (lane == 0) S.hw = hw;
+  __syncwarp();
+  return nc;
+}
+
+#ifndef LTS_BIG_WARP_ENTER
+#define LTS_BIG_WARP_ENTER 24  // a block step committing fewer keys enters warp mode
+#endif
+#ifndef LTS_BIG_WARP_EXIT
+#define LTS_BIG_WARP_EXIT 28   // a warp step committing this many returns to block mode
+#endif
+#ifndef LTS_BIG_WARP_FREE
+#define LTS_BIG_WARP_FREE 8    // ... or this many with no preemption
+#endif
 
 // One exact priority flood of a large region (the e-th extraction gets label
 // k-1-e for descending floods, e for ascending ones).  Each iteration commits
@@ -229,6 +363,12 @@ __device__ __forceinline__ void big_row(const BigRegion &G, int key, int (&q)[K]
 // order with the +-BIG sentinels of the first flood mapped to k and 0), so
 // the frontier ("leaf") and the seen set are bit sets over key space;
 // extracted = seen and not leaf.
+// The frontier rule runs in one of two modes.  Block mode: B = BIG_T
+// candidates from a chunk scan of the leaf words, block-wide scans (smooth
+// floods commit tens to hundreds of keys per step).  Warp mode: warp 0 alone
+// takes the top 32 keys through the frontier summary and runs the whole step
+// with shuffles and no block barrier (rough floods commit a few keys per
+// step, so the step latency is what counts).
 template <int K>
 __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, int *cout, int unused_key,
                           long long *dbg) {
@@ -243,11 +383,17 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     leaf[i] = 0u;
     seen[i] = 0u;
   }
+  for (int i = tid; i < S.nsw4; i += BIG_T) S.sum[i] = 0u;
+  const bool ks = S.nw4 > LTS_BIG_SUM_MIN_WORDS;
   if (tid == 0) {
+    S.keep_sum = ks;
+    S.hi_sw = -1;
+    S.hw = -1;
+    S.wmode = 0;
     S.hi_chunk = -1;
     S.ghi_chunk = k >> BIG_CHUNK_SHIFT;
     S.gblock = -1;
-    S.cut = 0x7fffffff;
+    S.cutbuf[0] = S.cutbuf[1] = 0x7fffffff;
   }
   __syncthreads();
   // the one key no slot maps to counts as extracted
@@ -258,8 +404,10 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     if (tid == 0) {
       const int key = flood_key(cin[0], false, k);
       seen[key >> 5] |= 1u << (key & 31);
-      leaf[key >> 5] |= 1u << (key & 31);
+      big_front_add(S, key, ks);
       S.hi_chunk = key >> BIG_CHUNK_SHIFT;
+      S.hi_sw = key >> 10;
+      S.hw = key >> 5;
       mine = 1;
     }
   } else {
@@ -268,13 +416,17 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
       if ((G.sfl[p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) {
         const int key = flood_key(cin[p], true, k);
         atomicOr(seen + (key >> 5), 1u << (key & 31));
-        atomicOr(leaf + (key >> 5), 1u << (key & 31));
-        mch = max(mch, key >> BIG_CHUNK_SHIFT);
+        big_front_add(S, key, ks);
+        mch = max(mch, key >> 5);
         mine = 1;
       }
     }
     mch = __reduce_max_sync(0xffffffffu, mch);
-    if (lane == 0 && mch >= 0) atomicMax(&S.hi_chunk, mch);
+    if (lane == 0 && mch >= 0) {
+      atomicMax(&S.hw, mch);
+      atomicMax(&S.hi_sw, mch >> 5);
+      atomicMax(&S.hi_chunk, mch >> (BIG_CHUNK_SHIFT - 5));
+    }
   }
   if (__syncthreads_or(mine) == 0) {  // empty ascending flood keeps the previous labels
     for (int p = tid; p < k; p += BIG_T) cout[p] = cin[p];
@@ -295,14 +447,24 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     }
     return make_uint4(w[0], w[1], w[2], w[3]);
   };
-  int e = 0;
-  long long nst = 0, ncand = 0, ngs = 0, ngc = 0;
+  int e = 0, par = 0;
+  long long nst = 0, ncand = 0, ngs = 0, ngc = 0, nga = 0, nws = 0;
+  long long tq = 0, tn;
+  if (dbg && tid == 0) tq = clock64();
+#define BIG_TICK(i)         \
+  if (dbg && tid == 0) {    \
+    tn = clock64();         \
+    dbg[i] += tn - tq;      \
+    tq = tn;                \
+  }
   while (e < k) {
     int key, q[K];
+    int *const cut = &S.cutbuf[par];
     // ---- (g) global rule ---------------------------------------------------
     int j = 0;
     const int gb = S.gblock;
     if (gb < 0 || big_bit(seen, gb)) {
+      nga++;
       const int ng = big_gather(S, S.ghi_chunk, unext4, key);
       const bool isc = tid < ng;
       int cand_p = 0;
@@ -313,15 +475,15 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
 #pragma unroll
         for (int kk = 0; kk < K; kk++) {
           const int x = q[kk];
-          if (x > key) ok = true;                                          // a higher neighbour
+          if (x > key) ok = true;                                               // a higher neighbour
           else if (x >= 0 && big_bit(seen, x) && !big_bit(leaf, x)) ok = true;  // an extracted one
-          if (x < 0 || big_bit(seen, x)) q[kk] = -1;                      // keep the exposures
+          if (x < 0 || big_bit(seen, x)) q[kk] = -1;                           // keep the exposures
         }
         const unsigned bad = __ballot_sync(__activemask(), !ok);
-        if (bad && lane == __ffs(bad) - 1) atomicMin(&S.cut, tid);
+        if (bad && lane == __ffs(bad) - 1) atomicMin(cut, tid);
       }
       __syncthreads();
-      j = min(S.cut, ng);
+      j = min(*cut, ng);
       if (j < ng && tid == j) S.gblock = key;  // first failing key: an unreached local maximum
       if (j == ng && tid == 0) S.gblock = -1;
       if (j > 0) {
@@ -334,26 +496,118 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
             const int x = q[kk];
             if (x >= 0) {
               atomicOr(seen + (x >> 5), 1u << (x & 31));
-              atomicOr(leaf + (x >> 5), 1u << (x & 31));
-              mch = max(mch, x >> BIG_CHUNK_SHIFT);
+              big_front_add(S, x, ks);
+              mch = max(mch, x >> 5);
             }
           }
         }
         mch = __reduce_max_sync(0xffffffffu, mch);
-        if (lane == 0 && mch >= 0) atomicMax(&S.hi_chunk, mch);
+        if (lane == 0 && mch >= 0) {
+          atomicMax(&S.hw, mch);
+          atomicMax(&S.hi_sw, mch >> 5);
+          atomicMax(&S.hi_chunk, mch >> (BIG_CHUNK_SHIFT - 5));
+        }
         __syncthreads();
         if (tid < j) atomicAnd(leaf + (key >> 5), ~(1u << (key & 31)));
         e += j;
         ngs++;
         ngc += j;
       }
+      if (tid == 0) S.cutbuf[par ^ 1] = 0x7fffffff;
+      par ^= 1;
       __syncthreads();
-      if (tid == 0) S.cut = 0x7fffffff;
-      __syncthreads();
+      BIG_TICK(17)
       if (j > 0) continue;
     }
-    // ---- (f) frontier rule ---------------------------------------------------
+    // ---- (f) frontier rule, warp mode ---------------------------------------
+    if (S.wmode) {
+      if (warp == 0) {
+        int ew = e;
+        long long wt = dbg ? clock64() : 0, wn;
+#define WARP_TICK(i)                         \
+  if (dbg) {                                 \
+    wn = clock64();                          \
+    if (lane == 0) dbg[i] += wn - wt;        \
+    wt = wn;                                 \
+  }
+        for (;;) {
+          int wkey;
+          const int nc = big_warp_gather(S, wkey);
+          WARP_TICK(20)
+          if (nc == 0) break;
+          int wq[K], cand_p = 0;
+          if (lane < nc) {
+            cand_p = G.inv[wkey];
+            big_row<K>(G, wkey, wq);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < K; kk++) wq[kk] = -1;
+          }
+          int nm = -1;
+#pragma unroll
+          for (int kk = 0; kk < K; kk++) {
+            const int x = wq[kk];
+            if (x >= 0 && !((((volatile uint32_t *)seen)[x >> 5] >> (x & 31)) & 1u)) nm = max(nm, x);
+            else wq[kk] = -1;
+          }
+          int inc = nm;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc = max(inc, y);
+          }
+          WARP_TICK(21)
+          int ex = __shfl_up_sync(0xffffffffu, inc, 1);
+          const unsigned bal = __ballot_sync(0xffffffffu, lane > 0 && lane < nc && ex > wkey);
+          const int jw = bal ? __ffs(bal) - 1 : nc;
+          int mch = -1;
+          if (lane < jw) {
+            cout[cand_p] = asc ? (ew + lane) : (k - 1 - (ew + lane));
+            atomicAnd(leaf + (wkey >> 5), ~(1u << (wkey & 31)));
+#pragma unroll
+            for (int kk = 0; kk < K; kk++) {
+              const int x = wq[kk];
+              if (x >= 0) {
+                atomicOr(seen + (x >> 5), 1u << (x & 31));
+                big_front_add(S, x, ks);
+                mch = max(mch, x >> 5);
+              }
+            }
+          }
+          mch = __reduce_max_sync(0xffffffffu, mch);
+          if (lane == 0 && mch >= 0) {
+            S.hw = max(S.hw, mch);
+            S.hi_sw = max(S.hi_sw, mch >> 5);
+            S.hi_chunk = max(S.hi_chunk, mch >> (BIG_CHUNK_SHIFT - 5));
+          }
+          __syncwarp();
+          __threadfence_block();
+          WARP_TICK(22)
+          ew += jw;
+          nws++;
+          // back to block mode once the flood commits (nearly) a whole warp's
+          // candidates, or commits every candidate of a window without a
+          // preemption (a smooth phase in a sparse frontier: block steps
+          // would commit more keys per step)
+          if (ew >= k || jw >= LTS_BIG_WARP_EXIT || (jw == nc && nc >= LTS_BIG_WARP_FREE)) break;
+          const int gbw = S.gblock;
+          if (gbw >= 0 && ((((volatile uint32_t *)seen)[gbw >> 5] >> (gbw & 31)) & 1u)) break;
+        }
+#undef WARP_TICK
+        if (lane == 0) {
+          S.ew = ew;
+          S.wmode = 0;
+        }
+      }
+      __syncthreads();
+      e = S.ew;
+      BIG_TICK(19)
+      continue;
+    }
+    // ---- (f) frontier rule, block mode --------------------------------------
+    int *const cutf = &S.cutbuf[par];
     const int nc = big_gather(S, S.hi_chunk, leaf4, key);
+    BIG_TICK(8)
     if (nc == 0) break;
     const bool isc = tid < nc;
     int cand_p = 0;
@@ -371,6 +625,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
       if (x >= 0 && !big_bit(seen, x)) nm = max(nm, x);
       else q[kk] = -1;
     }
+    BIG_TICK(9)
     // first preemption: exclusive prefix max of the exposures in candidate
     // order against the candidate's own key
     {
@@ -389,10 +644,11 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
       int ex = __shfl_up_sync(0xffffffffu, inc, 1);
       ex = lane == 0 ? pre : max(pre, ex);
       const unsigned bal = __ballot_sync(0xffffffffu, isc && tid > 0 && ex > key);
-      if (lane == 0 && bal) atomicMin(&S.cut, warp * 32 + __ffs(bal) - 1);
+      if (lane == 0 && bal) atomicMin(cutf, warp * 32 + __ffs(bal) - 1);
       __syncthreads();
     }
-    j = min(S.cut, nc);
+    j = min(*cutf, nc);
+    BIG_TICK(10)
     // commit the prefix: labels, leave F; its exposures join F (setting a bit
     // twice is harmless, so the updates need no return value)
     int mch = -1;
@@ -404,13 +660,17 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
         const int x = q[kk];
         if (x >= 0) {
           atomicOr(seen + (x >> 5), 1u << (x & 31));
-          atomicOr(leaf + (x >> 5), 1u << (x & 31));
-          mch = max(mch, x >> BIG_CHUNK_SHIFT);
+          big_front_add(S, x, ks);
+          mch = max(mch, x >> 5);
         }
       }
     }
     mch = __reduce_max_sync(0xffffffffu, mch);
-    if (lane == 0 && mch >= 0) atomicMax(&S.hi_chunk, mch);
+    if (lane == 0 && mch >= 0) {
+      atomicMax(&S.hw, mch);
+      atomicMax(&S.hi_sw, mch >> 5);
+      atomicMax(&S.hi_chunk, mch >> (BIG_CHUNK_SHIFT - 5));
+    }
     e += j;
     nst++;
     ncand += nc;
@@ -419,18 +679,24 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
       dbg[13] += j <= 32;
       dbg[14] += (j + 31) / 32;
       dbg[15] += j == nc;
-      dbg[16] += (j + 63) / 64;
     }
+    if (tid == 0) {
+      S.cutbuf[par ^ 1] = 0x7fffffff;
+      if (j < LTS_BIG_WARP_ENTER) S.wmode = 1;
+    }
+    par ^= 1;
     __syncthreads();
-    if (tid == 0) S.cut = 0x7fffffff;
-    __syncthreads();
+    BIG_TICK(11)
   }
+#undef BIG_TICK
   if (dbg && tid == 0) {
     dbg[1] += nst;
     dbg[2] += ncand;
     dbg[3] += e;
     dbg[5] += ngs;
     dbg[6] += ngc;
+    dbg[16] += nws;
+    dbg[18] += nga;
   }
 }
 
@@ -439,7 +705,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
 // (_kernels.py:453-481).  grid.y = big-region index, grid.x = slot chunks.
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_big_rows(LocArgs A, BigArgs Bg) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   const int n = (int)A.g.n;
   const int lane = threadIdx.x & 31;
   // flat over the slots of all big regions; warps stay converged so the
@@ -454,13 +720,12 @@ __global__ void __launch_bounds__(256) k_big_rows(LocArgs A, BigArgs Bg) {
       const int p = i - Bg.bpre[qi];
       const int s = A.verts[lo];
       const int srank = eff_rank(A.rank, s, A.rev, n);
-      int x, y, z;
-      coords(A.g, A.verts[lo + p], x, y, z);
+      const Nb<NDIM> nb(A.g, A.verts[lo + p]);
       bool out = false;
       int *row = Bg.nrow + ((size_t)lo + p) * K;
 #pragma unroll
       for (int kk = 0; kk < K; kk++) {
-        int u = nbr_at(A.g, x, y, z, kk);
+        int u = nb(A.g, kk);
         row[kk] = member(A, u, rid, s);
         if (p >= 1 && u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) out = true;
       }
@@ -561,7 +826,7 @@ __global__ void k_big_init(LocArgs A, BigArgs Bg) {
 // One row per thread, the K label gathers of a row independent of each other.
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_big_setup(LocArgs A, BigArgs Bg) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   static_assert(K % 2 == 0, "rows are read and written as int2");
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Bg.bslots; i += gridDim.x * blockDim.x) {
     const int qi = big_locate(Bg, i);
@@ -596,7 +861,7 @@ __global__ void __launch_bounds__(256) k_big_setup(LocArgs A, BigArgs Bg) {
 // one CTA per region (grid = regions, largest first): flood t -> t+1
 template <int NDIM>
 __global__ void __launch_bounds__(BIG_T) k_big_flood(LocArgs A, BigArgs Bg) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   extern __shared__ __align__(16) unsigned char smraw[];
   BigSmem &S = *reinterpret_cast<BigSmem *>(smraw);
   const int tid = threadIdx.x;
@@ -619,12 +884,21 @@ __global__ void __launch_bounds__(BIG_T) k_big_flood(LocArgs A, BigArgs Bg) {
   // candidate scan reads them every step), else in the region's spill space
   if (tid == 0) {
     const int nw = (k + 1 + 31) >> 5;
-    uint32_t *gp = Bg.gbits + ((3 * (((size_t)lo + rid + 31) >> 5) + 8 * (size_t)rid + 3) & ~(size_t)3);
+    // spill space: leaf, seen and summary words of every region fit in
+    // 3 (k+1)/32 + 16 words per region (gbits holds 6n + 64 words)
+    uint32_t *gp = Bg.gbits + ((3 * (((size_t)lo + rid) >> 5) + 16 * (size_t)rid + 3) & ~(size_t)3);
     const int nw4 = (nw + 3) & ~3;  // leaf read as uint4; padding stays zero
+    const int nsw4 = (((nw + 31) >> 5) + 3) & ~3;
+    S.nsw4 = nsw4;
     S.nw = nw;
     S.nw4 = nw4;
-    S.leaf = nw4 <= BIG_SMEM_WORDS ? S.bits : gp;
-    S.seen = 2 * nw4 <= BIG_SMEM_WORDS ? S.bits + nw4 : gp + nw4;
+    // shared memory in order of use per step: summary, leaf, seen
+    int used = 0;
+    S.sum = nsw4 <= BIG_SMEM_WORDS ? S.bits : gp + 2 * nw4;
+    if (nsw4 <= BIG_SMEM_WORDS) used = nsw4;
+    S.leaf = used + nw4 <= BIG_SMEM_WORDS ? S.bits + used : gp;
+    if (used + nw4 <= BIG_SMEM_WORDS) used += nw4;
+    S.seen = used + nw4 <= BIG_SMEM_WORDS ? S.bits + used : gp + nw4;
   }
   __syncthreads();
   const int qa = Bg.qbase + qi;  // absolute big-queue position
@@ -644,7 +918,7 @@ __global__ void __launch_bounds__(BIG_T) k_big_flood(LocArgs A, BigArgs Bg) {
 // besides the saddle) and, from t+1 >= 3 on, state t+1 != state t-1
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_big_check(LocArgs A, BigArgs Bg) {
-  constexpr int K = NDIM == 2 ? 6 : 14;
+  constexpr int K = KOf<NDIM>::value;
   const int lane = threadIdx.x & 31;
   for (int b0 = blockIdx.x * blockDim.x; b0 < Bg.bslots; b0 += gridDim.x * blockDim.x) {
     const int i = b0 + threadIdx.x;

@@ -31,10 +31,14 @@ constexpr uint8_t FL_MAX = 2;   // no upper neighbour  (upper link empty)
 constexpr uint8_t PM_MIN = 1;   // preserved minimum mark
 constexpr uint8_t PM_MAX = 2;   // preserved maximum mark
 
+// The mesh: a regular 2D/3D Freudenthal grid (ndim 2/3, implicit stencil) or
+// an explicit triangle mesh (ndim 0: symmetric CSR adjacency cptr/cidx, as the
+// reference's Triangulation.indptr/indices, triangulation.py:81-125).
 struct Grid {
-  int nx, ny, nz;  // nz == 1 in 2D
+  int nx, ny, nz;  // nz == 1 in 2D; explicit mesh: nx = n, ny = nz = 1
   int ndim, K;
   int64_t n;
+  const int *cptr, *cidx;  // explicit mesh only
 };
 
 // stencil offsets, x/y/z per neighbour (reference triangulation.py:32-45)
@@ -54,6 +58,36 @@ __device__ __forceinline__ int nbr_at(const Grid &g, int x, int y, int z, int k)
     return -1;
   return a + g.nx * (b + g.ny * c);
 }
+
+#ifndef LTS_CSR_K
+#define LTS_CSR_K 16
+#endif
+constexpr int kCsrK = LTS_CSR_K;  // largest vertex degree of explicit meshes
+
+// neighbour slots per vertex: 6 / 14 grid stencil entries, kCsrK CSR entries
+template <int NDIM>
+struct KOf {
+  static constexpr int value = NDIM == 2 ? 6 : (NDIM == 3 ? 14 : kCsrK);
+};
+
+// the neighbours of one vertex, slot k = 0..K-1 (-1: no neighbour in that slot)
+template <int NDIM>
+struct Nb {
+  int a, b, c;  // grid: x, y, z; explicit mesh: row start, degree
+  __device__ __forceinline__ Nb(const Grid &g, int v) {
+    if (NDIM == 0) {
+      a = g.cptr[v];
+      b = g.cptr[v + 1] - a;
+      c = 0;
+    } else {
+      coords(g, v, a, b, c);
+    }
+  }
+  __device__ __forceinline__ int operator()(const Grid &g, int k) const {
+    if (NDIM == 0) return k < b ? g.cidx[a + k] : -1;
+    return nbr_at(g, a, b, c, k);
+  }
+};
 
 // effective rank of the current pass: the minima pass runs the maxima
 // machinery on the reversed order n-1-rank (reference order.py:54-56)

@@ -28,6 +28,7 @@
 #include "localize_big.cuh"
 #include "integrate.cuh"
 #include "persistence.cuh"
+#include "csr.cuh"
 
 namespace lts {
 int64_t g_launches = 0;
@@ -262,7 +263,8 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   auto i32 = [&](int64_t cnt) { return (int *)take(sizeof(int) * (size_t)cnt); };
   auto u32 = [&](int64_t cnt) { return (uint32_t *)take(sizeof(uint32_t) * (size_t)cnt); };
   int64_t n1 = n + 1, s2 = 2 * n + 2;
-  int KH = ndim == 2 ? 3 : 7;
+  // maxima-graph edge capacity per vertex (explicit meshes: one per mesh edge end)
+  int KH = ndim == 2 ? 3 : (ndim == 3 ? 7 : kCsrK);
   w->rankA = i32(n); w->invA = i32(n); w->rankB = i32(n); w->invB = i32(n);
   w->ptr = i32(n); w->M = i32(n); w->rt = i32(n); w->acc = i32(n); w->comp = i32(n); w->par = i32(n); w->wc = i32(n);
   w->rpar = i32(n); w->ridx = i32(n); w->reg_of = i32(n); w->loc_of = i32(n);
@@ -288,8 +290,9 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->bpre = i32(n1 / BIG_THRESHOLD + 4);
   w->cbits = u32(n / 32 + 64);
   w->gbits = u32(6 * n + 64);
-  w->nrow = i32((ndim == 2 ? 6 : 14) * s2);
-  w->nrowkey = i32((ndim == 2 ? 6 : 14) * s2);
+  const int KR = ndim == 2 ? 6 : (ndim == 3 ? 14 : kCsrK);  // neighbour slots per region slot
+  w->nrow = i32(KR * s2);
+  w->nrowkey = i32(KR * s2);
   w->sb.k1 = u32(n); w->sb.v1 = u32(n); w->sb.k2 = u32(n); w->sb.v2 = u32(n);
   w->sb.status = u32(rs::status_elems(n));
   w->sb.hist = u32(4 * 256);
@@ -314,7 +317,16 @@ struct Ctx {
   bool timing;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
   int64_t flood_launches = 0, flood_slots = 0;
+  const int *lptr = nullptr, *la = nullptr, *lb = nullptr;  // explicit mesh: link edges (counts only)
 };
+
+// classification of the pass's order: stencil kernels on grids, the CSR
+// kernel on explicit meshes
+static void classify_any(Ctx &c, const int32_t *rank, uint8_t *flags, int16_t *lower, int16_t *upper,
+                         const uint8_t *lut, int32_t *ptr, int ptr_kind, cudaStream_t s) {
+  if (c.g.ndim == 0) launch_classify_csr(c.g, rank, flags, lower, upper, c.lptr, c.la, c.lb, ptr, ptr_kind, s);
+  else launch_classify(c.g, rank, flags, lower, upper, lut, ptr, ptr_kind, s);
+}
 
 static cudaEvent_t next_event() {
   DevState &d = *g_cur;
@@ -358,7 +370,60 @@ static int bits_for(int64_t maxval) {
   return b;
 }
 
+static int setup_common(Ctx &c, void *ws, size_t ws_bytes, void *stream) {
+  c.s = (cudaStream_t)stream;
+  LTS_TRY(select_device());
+  int64_t need = carve(&c.w, nullptr, c.g.ndim, c.n);
+  if (ws != nullptr) {
+    if ((size_t)need > ws_bytes) return lts_set_error(LTS_E_WORKSPACE, "workspace too small");
+    carve(&c.w, (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255), c.g.ndim, c.n);
+  }
+  LTS_TRY(init_tables());
+  if (!g_cur->h_scal) LTS_CUDA(cudaHostAlloc((void **)&g_cur->h_scal, sizeof(int) * SC_N, cudaHostAllocDefault));
+  c.h_scal = g_cur->h_scal;
+  c.timing = false;
+  g_cur->ev_next = 0;
+  return 0;
+}
+
+// An explicit triangle mesh: n vertices, symmetric CSR
+// adjacency (device int32 indptr[n+1], indices[nnz]), every degree <= kCsrK.
+static int setup_csr(Ctx &c, int64_t n, const int32_t *indptr, const int32_t *indices, void *ws, size_t ws_bytes,
+                     void *stream) {
+  if (n < 1 || n > ((int64_t)1 << 30)) return lts_set_error(LTS_E_BAD_DIMS, "mesh needs 1 <= n <= 2^30 vertices");
+  if (!indptr || !indices) return lts_set_error(LTS_E_INVALID, "indptr and indices are required");
+  c.g.nx = (int)n;
+  c.g.ny = 1;
+  c.g.nz = 1;
+  c.g.ndim = 0;
+  c.g.K = kCsrK;
+  c.g.n = n;
+  c.g.cptr = indptr;
+  c.g.cidx = indices;
+  c.n = n;
+  LTS_TRY(setup_common(c, ws, ws_bytes, stream));
+  c.lut = nullptr;
+  if (ws) {  // the device rows hold kCsrK neighbours per vertex
+    LTS_CUDA(cudaMemsetAsync(c.w.scal + SC_TMP, 0, sizeof(int), c.s));
+    k_max_degree<<<grid_blocks(n, 256), 256, 0, c.s>>>(indptr, n, c.w.scal + SC_TMP);
+    g_launches++;
+    LTS_TRY(readback(c, SC_TMP, 1));
+    if (c.h_scal[SC_TMP] > kCsrK) return lts_set_error(LTS_E_BAD_DIMS, "a vertex has more than LTS_CSR_K (16) neighbours");
+  }
+  return 0;
+}
+
 static int setup(Ctx &c, int ndim, const int64_t *dims, void *ws, size_t ws_bytes, void *stream) {
+  c.g.cptr = c.g.cidx = nullptr;
+  if (ndim == 1) {  // a plain vertex list (order field of an explicit mesh)
+    if (dims[0] < 1 || dims[0] > ((int64_t)1 << 30)) return lts_set_error(LTS_E_BAD_DIMS, "need 1 <= n <= 2^30 vertices");
+    c.g.nx = (int)dims[0];
+    c.g.ny = c.g.nz = 1;
+    c.g.ndim = 1;
+    c.g.K = 0;
+    c.g.n = c.n = dims[0];
+    return setup_common(c, ws, ws_bytes, stream);
+  }
   if (ndim != 2 && ndim != 3) return lts_set_error(LTS_E_BAD_DIMS, "grid must be 2D or 3D");
   int64_t n = 1;
   for (int a = 0; a < ndim; a++) {
@@ -432,11 +497,13 @@ static int big_stream_fork(cudaStream_t s) {
   if (!d.big_attr) {
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
+    LTS_CUDA(cudaFuncSetAttribute(k_big_flood<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
     // leave the rest of the unified L1/shared array to L1: the floods re-read
     // region rows and keys that fit there
     int carve = (int)((sizeof(BigSmem) * 100 + 227 * 1024 - 1) / (228 * 1024)) + 1;
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<3>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    LTS_CUDA(cudaFuncSetAttribute(k_big_flood<0>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     d.big_attr = true;
   }
   // LTS_BIG_SERIAL (diagnostic): run the large-region floods on the main
@@ -462,7 +529,8 @@ static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
   const int rg = gx;
   LTS_CUDA(cudaMemsetAsync(B.nactive, 0, sizeof(int), g_bigs));
   if (c.g.ndim == 2) k_big_setup<2><<<rg, 256, 0, g_bigs>>>(A, B);
-  else k_big_setup<3><<<rg, 256, 0, g_bigs>>>(A, B);
+  else if (c.g.ndim == 3) k_big_setup<3><<<rg, 256, 0, g_bigs>>>(A, B);
+  else k_big_setup<0><<<rg, 256, 0, g_bigs>>>(A, B);
   // device time of the flood kernel itself (report slot LTS_PH_FLOOD_KERNEL)
   cudaEvent_t fa = nullptr, fb = nullptr;
   if (c.timing) {
@@ -470,18 +538,17 @@ static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
     LTS_CUDA(cudaEventRecord(fa, g_bigs));
   }
   if (c.g.ndim == 2) k_big_flood<2><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
-  else k_big_flood<3><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+  else if (c.g.ndim == 3) k_big_flood<3><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+  else k_big_flood<0><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
   if (c.timing) {
     fb = next_event();
     LTS_CUDA(cudaEventRecord(fb, g_bigs));
     c.marks.push_back({LTS_PH_FLOOD_KERNEL, {fa, fb}});
     c.flood_launches++;
   }
-  if (c.g.ndim == 2) {
-    k_big_check<2><<<rg, 256, 0, g_bigs>>>(A, B);
-  } else {
-    k_big_check<3><<<rg, 256, 0, g_bigs>>>(A, B);
-  }
+  if (c.g.ndim == 2) k_big_check<2><<<rg, 256, 0, g_bigs>>>(A, B);
+  else if (c.g.ndim == 3) k_big_check<3><<<rg, 256, 0, g_bigs>>>(A, B);
+  else k_big_check<0><<<rg, 256, 0, g_bigs>>>(A, B);
   k_big_decide<<<NB(B.nbig), 256, 0, g_bigs>>>(A, B);
   g_launches += 4;
   LTS_KCHECK();
@@ -507,7 +574,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
   {
     Phase ph(c, LTS_PH_CLASSIFY);
     if (!classified)
-      launch_classify(c.g, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
+      classify_any(c, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
     LTS_KCHECK();
   }
   {
@@ -554,7 +621,9 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         LTS_CUDA(cudaMemsetAsync(w.scal + SC_ECOUNT, 0, sizeof(int) * 2, s));
         LTS_CUDA(cudaMemsetAsync(w.bestP, 0, sizeof(unsigned long long) * n, s));
       }
-      {
+      if (c.g.ndim == 0) {
+        k_edges_csr<<<NB(n), 256, 0, s>>>(c.g, rank, rev, w.M, w.vcls, ea, eb, ew, w.scal + SC_ECOUNT, w.bestP, H);
+      } else {
         dim3 eg((c.g.nx + ET_TX - 1) / ET_TX, (c.g.ny + ET_TY - 1) / ET_TY,
                 c.g.ndim == 2 ? 1 : (c.g.nz + ET_ZC - 1) / ET_ZC);
         dim3 eb3(ET_TX, ET_TY);
@@ -664,7 +733,8 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       // flat kernels over all big-region slots
       big_gx = (int)std::min<int64_t>((B.bslots + 255) / 256, 148 * 8);
       if (c.g.ndim == 2) k_big_rows<2><<<big_gx, 256, 0, g_bigs>>>(A, B);
-      else k_big_rows<3><<<big_gx, 256, 0, g_bigs>>>(A, B);
+      else if (c.g.ndim == 3) k_big_rows<3><<<big_gx, 256, 0, g_bigs>>>(A, B);
+      else k_big_rows<0><<<big_gx, 256, 0, g_bigs>>>(A, B);
       k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B);
       g_launches += 4;
       LTS_TRY(big_iteration(c, A, B, big_gx));
@@ -674,7 +744,8 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       int blocks = (R - nbig + LOC_WARPS - 1) / LOC_WARPS;
       if (blocks > 148 * 8) blocks = 148 * 8;
       if (c.g.ndim == 2) k_localize<2><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
-      else k_localize<3><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
+      else if (c.g.ndim == 3) k_localize<3><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
+      else k_localize<0><<<blocks, 32 * LOC_WARPS, 0, s>>>(A);
       g_launches++;
     }
     // Work that does not need the local orders runs while the large-region
@@ -835,7 +906,7 @@ static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, i
   // every extremum of the polarity is a seed: no preserve marks
   LTS_CUDA(cudaMemsetAsync(w.pmark, 0, (size_t)n, s));
   LTS_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(int) * SC_N, s));
-  launch_classify(c.g, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
+  classify_any(c, rank, w.flags, nullptr, nullptr, c.lut, w.ptr, kind == 0 ? PTR_ASC : PTR_DESC, s);
   k_mark_maxima<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, kind, n, w.vcls, w.cst, w.mlist, w.scal + SC_COUNTS,
                                        w.comp, w.par, w.acc, w.rpar, w.bestP);
   for (int j = 0; j < LTS_JUMPS; j++) k_jump<<<NB(n), 256, 0, s>>>(w.ptr, n);
@@ -948,7 +1019,9 @@ static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, i
       int *sa = w.verts, *sb2 = w.out, *sw = (int *)w.gheap;
       k_pn_gather_rest<<<NB(rem), 256, 0, s>>>(w.oval, rem, pa, pb, pw, map, sa, sb2, sw);
       const size_t shm = sizeof(int) * (size_t)nm2;
-      const int use_smem = shm <= 220 * 1024;
+      // LTS_PAIRS_FORCE_GLOBAL (test hook): run the global-memory branch of
+      // the sweep on fields whose forest would fit in shared memory
+      const int use_smem = shm <= 220 * 1024 && getenv("LTS_PAIRS_FORCE_GLOBAL") == nullptr;
       if (use_smem)
         LTS_CUDA(cudaFuncSetAttribute(k_pn_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
       k_pn_sweep<<<1, 256, use_smem ? shm : 0, s>>>(sa, sb2, sw, rem, nrank2, nm2, par, use_smem, (int *)w.skey,
@@ -1012,7 +1085,7 @@ int lts_bench_kernels(const float *f, int ndim, const int64_t *dims, int reps, d
     // classification, flags only
     LTS_CUDA(cudaMemsetAsync(flush, r & 0xff, fb, s));
     LTS_CUDA(cudaEventRecord(a, s));
-    launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
+    classify_any(c, w.rankA, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
     LTS_CUDA(cudaEventRecord(b, s));
     LTS_CUDA(cudaEventSynchronize(b));
     LTS_CUDA(cudaEventElapsedTime(&ms, a, b));
@@ -1020,7 +1093,7 @@ int lts_bench_kernels(const float *f, int ndim, const int64_t *dims, int reps, d
     // classification + ascent pointer
     LTS_CUDA(cudaMemsetAsync(flush, r & 0xff, fb, s));
     LTS_CUDA(cudaEventRecord(a, s));
-    launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, w.ptr, PTR_ASC, s);
+    classify_any(c, w.rankA, w.flags, nullptr, nullptr, c.lut, w.ptr, PTR_ASC, s);
     LTS_CUDA(cudaEventRecord(b, s));
     LTS_CUDA(cudaEventSynchronize(b));
     LTS_CUDA(cudaEventElapsedTime(&ms, a, b));
@@ -1130,7 +1203,7 @@ int lts_classify(const int32_t *rank, int ndim, const int64_t *dims, uint8_t *fl
   Ctx c;
   LTS_TRY(setup(c, ndim, dims, nullptr, 0, stream));
   if ((lower == nullptr) != (upper == nullptr)) return lts_set_error(LTS_E_INVALID, "lower and upper go together");
-  launch_classify(c.g, rank, flags, lower, upper, c.lut, nullptr, PTR_NONE, c.s);
+  classify_any(c, rank, flags, lower, upper, c.lut, nullptr, PTR_NONE, c.s);
   LTS_KCHECK();
   return 0;
 }
@@ -1148,12 +1221,9 @@ int lts_remove_pass(int kind, const int32_t *rank, const int32_t *inverse, const
   return run_pass(c, kind, rank, inverse, pmark, max_iterations, new_rank, new_inverse, g, rep, view);
 }
 
-int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *pres_max, int64_t n_max,
-                 const int64_t *pres_min, int64_t n_min, const int32_t *order, float *g, int32_t *G,
-                 lts_report_t *rep, const lts_options_t *opt, void *ws, size_t ws_bytes, void *stream) {
-  LTS_LOCK;
-  Ctx c;
-  LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
+static int simplify_impl(Ctx &c, const float *f, const int64_t *pres_max, int64_t n_max, const int64_t *pres_min,
+                         int64_t n_min, const int32_t *order, float *g, int32_t *G, lts_report_t *rep,
+                         const lts_options_t *opt, void *ws) {
   if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
   if ((f == nullptr) != (g == nullptr)) return lts_set_error(LTS_E_INVALID, "f and g go together");
   if (!f && !order) return lts_set_error(LTS_E_INVALID, "f is required unless an order field is given");
@@ -1188,7 +1258,7 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
   {
     // extrema of F; the ascent pointers are the first maxima pass's input
     Phase ph(c, LTS_PH_CLASSIFY);
-    launch_classify(c.g, w.rankA, w.flags, nullptr, nullptr, c.lut, w.ptr, PTR_ASC, s);
+    classify_any(c, w.rankA, w.flags, nullptr, nullptr, c.lut, w.ptr, PTR_ASC, s);
   }
   k_check_pres<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, w.scal + SC_BADPRES);
   if (g) k_copy_canon<<<NB(n), 256, 0, s>>>(f, g, n);
@@ -1219,7 +1289,7 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
     }
     // restore (D6) and verify
     Phase ph(c, LTS_PH_VERIFY);
-    launch_classify(c.g, cr, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
+    classify_any(c, cr, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
     LTS_CUDA(cudaMemsetAsync(w.scal + SC_VERIFY, 0, sizeof(int) * 4, s));
     k_verify<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, w.scal + SC_VERIFY);
     g_launches++;
@@ -1239,7 +1309,8 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
         LTS_CUDA(cudaStreamSynchronize(s));
         std::sort(ids.begin(), ids.end());
         for (int x : ids) {
-          if (c.g.ndim == 2) k_restore_target<2><<<1, 32, 0, s>>>(c.g, cr, x, kind, w.scal + SC_RESTORE);
+          if (c.g.ndim == 0) k_restore_target<0><<<1, 32, 0, s>>>(c.g, cr, x, kind, w.scal + SC_RESTORE);
+          else if (c.g.ndim == 2) k_restore_target<2><<<1, 32, 0, s>>>(c.g, cr, x, kind, w.scal + SC_RESTORE);
           else k_restore_target<3><<<1, 32, 0, s>>>(c.g, cr, x, kind, w.scal + SC_RESTORE);
           k_restore_shift<<<NB(n), 256, 0, s>>>(cr, n, x, kind, w.scal + SC_RESTORE);
           g_launches += 2;
@@ -1247,7 +1318,7 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
         R.restored += nl;
       }
       k_scatter_inverse<<<NB(n), 256, 0, s>>>(cr, ci, n);
-      launch_classify(c.g, cr, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
+      classify_any(c, cr, w.flags, nullptr, nullptr, c.lut, nullptr, PTR_NONE, s);
       LTS_CUDA(cudaMemsetAsync(w.scal + SC_VERIFY, 0, sizeof(int) * 4, s));
       k_verify<<<NB(n), 256, 0, s>>>(w.flags, w.pmark, n, w.scal + SC_VERIFY);
       g_launches += 2;
@@ -1287,6 +1358,65 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
   if (rep) *rep = R;
   if (!ok) return lts_set_error(LTS_E_VERIFY_FAILED_AT_CAP, "verify_constraints still failing after maxIterations outer iterations");
   return 0;
+}
+
+int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *pres_max, int64_t n_max,
+                 const int64_t *pres_min, int64_t n_min, const int32_t *order, float *g, int32_t *G,
+                 lts_report_t *rep, const lts_options_t *opt, void *ws, size_t ws_bytes, void *stream) {
+  LTS_LOCK;
+  Ctx c;
+  LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
+  return simplify_impl(c, f, pres_max, n_max, pres_min, n_min, order, g, G, rep, opt, ws);
+}
+
+// ---------------------------------------------------------------------------
+// explicit triangle meshes: the same pass over a CSR mesh
+// ---------------------------------------------------------------------------
+int lts_workspace_size_csr(int64_t n, size_t *bytes) {
+  if (n < 1 || n > ((int64_t)1 << 30)) return lts_set_error(LTS_E_BAD_DIMS, "mesh needs 1 <= n <= 2^30 vertices");
+  WS w;
+  *bytes = (size_t)carve(&w, nullptr, 0, n) + 256;
+  return 0;
+}
+
+int lts_classify_csr(const int32_t *rank, int64_t n, const int32_t *indptr, const int32_t *indices,
+                     const int32_t *link_ptr, const int32_t *link_a, const int32_t *link_b, uint8_t *flags,
+                     int16_t *lower, int16_t *upper, void *stream) {
+  LTS_LOCK;
+  Ctx c;
+  LTS_TRY(setup_csr(c, n, indptr, indices, nullptr, 0, stream));
+  if ((lower == nullptr) != (upper == nullptr)) return lts_set_error(LTS_E_INVALID, "lower and upper go together");
+  if (lower && !(link_ptr && link_a && link_b))
+    return lts_set_error(LTS_E_INVALID, "link_ptr / link_a / link_b are required for the component counts");
+  c.lptr = link_ptr;
+  c.la = link_a;
+  c.lb = link_b;
+  classify_any(c, rank, flags, lower, upper, nullptr, nullptr, PTR_NONE, c.s);
+  LTS_KCHECK();
+  return 0;
+}
+
+int lts_remove_pass_csr(int kind, const int32_t *rank, const int32_t *inverse, const uint8_t *pmark, int64_t n,
+                        const int32_t *indptr, const int32_t *indices, int32_t max_iterations, int32_t *new_rank,
+                        int32_t *new_inverse, float *g, lts_pass_report_t *rep, lts_regions_view_t *view, void *ws,
+                        size_t ws_bytes, void *stream) {
+  LTS_LOCK;
+  Ctx c;
+  LTS_TRY(setup_csr(c, n, indptr, indices, ws, ws_bytes, stream));
+  if (!ws) return lts_set_error(LTS_E_WORKSPACE, "workspace required");
+  if (kind != 0 && kind != 1) return lts_set_error(LTS_E_INVALID, "kind must be 0 (maxima) or 1 (minima)");
+  if (max_iterations < 1) max_iterations = 100;
+  return run_pass(c, kind, rank, inverse, pmark, max_iterations, new_rank, new_inverse, g, rep, view);
+}
+
+int lts_simplify_csr(const float *f, int64_t n, const int32_t *indptr, const int32_t *indices,
+                     const int64_t *pres_max, int64_t n_max, const int64_t *pres_min, int64_t n_min,
+                     const int32_t *order, float *g, int32_t *G, lts_report_t *rep, const lts_options_t *opt,
+                     void *ws, size_t ws_bytes, void *stream) {
+  LTS_LOCK;
+  Ctx c;
+  LTS_TRY(setup_csr(c, n, indptr, indices, ws, ws_bytes, stream));
+  return simplify_impl(c, f, pres_max, n_max, pres_min, n_min, order, g, G, rep, opt, ws);
 }
 
 }  // extern "C"

@@ -104,6 +104,12 @@ class VerifyReport:
     lost_minima: torch.Tensor
 
 
+def _workspace(mesh: Triangulation, dev):
+    if mesh.is_grid:
+        return N.workspace(mesh.grid_dims, dev)
+    return N.workspace(None, dev, explicit_n=mesh.n)
+
+
 def _ids(x, device) -> torch.Tensor:
     if x is None:
         return torch.empty(0, dtype=torch.int64, device=device)
@@ -156,7 +162,7 @@ def simplify_raw(mesh: Triangulation, values: Optional[torch.Tensor], pres_max: 
     if values is not None:
         g = g_out if g_out is not None else torch.empty(mesh.n, dtype=torch.float32, device=dev)
     G = G_out if G_out is not None else torch.empty(mesh.n, dtype=torch.int32, device=dev)
-    ws = N.workspace(mesh.grid_dims, dev)
+    ws = _workspace(mesh, dev)
     opt = N.lts_options_t()
     opt.max_iterations = int(options.maxIterations)
     opt.restore_interior_extrema = 1 if options.restoreInteriorExtrema else 0
@@ -166,11 +172,14 @@ def simplify_raw(mesh: Triangulation, values: Optional[torch.Tensor], pres_max: 
         opt.region_ni_capacity = ni_out.numel()
     rep = N.lts_report_t()
     with torch.cuda.device(dev):
-        rc = N.load().lts_simplify(N.ptr(values), mesh.dim, N.dims_arg(mesh.grid_dims), N.ptr(pres_max),
-                                   pres_max.numel(), N.ptr(pres_min), pres_min.numel(),
-                                   N.ptr(order) if order is not None else None, N.ptr(g), N.ptr(G),
-                                   ctypes.byref(rep), ctypes.byref(opt), N.ptr(ws), ws.numel(),
-                                   N.stream_ptr(dev))
+        tail = (N.ptr(pres_max), pres_max.numel(), N.ptr(pres_min), pres_min.numel(),
+                N.ptr(order) if order is not None else None, N.ptr(g), N.ptr(G),
+                ctypes.byref(rep), ctypes.byref(opt), N.ptr(ws), ws.numel(), N.stream_ptr(dev))
+        if mesh.is_grid:
+            rc = N.load().lts_simplify(N.ptr(values), mesh.dim, N.dims_arg(mesh.grid_dims), *tail)
+        else:
+            d = mesh.device_arrays(dev)
+            rc = N.load().lts_simplify_csr(N.ptr(values), mesh.n, N.ptr(d["indptr"]), N.ptr(d["indices"]), *tail)
     N.check(rc)
     return g, G, rep
 
@@ -195,7 +204,7 @@ def simplify_field(mesh: Triangulation, f, constraints: ConstraintSet,
         gf = realize_numeric(f, Gf, options.zeta)
         report.linf = float((gf.values - f.values.to(torch.float64)).abs().max()) if mesh.n else 0.0
         return gf, Gf, report
-    report.linf = float((g - f.values).abs().max()) if mesh.n else 0.0
+    report.linf = float((g.to(torch.float64) - f.values.to(torch.float64)).abs().max()) if mesh.n else 0.0
     return ScalarField._wrap(mesh, g), Gf, report
 
 
@@ -261,14 +270,18 @@ def remove_pass(mesh: Triangulation, F: OrderField, preserve: ConstraintSet, kin
     inv = F.inverse32 if F.inverse32 is not None else F.inverse.to(torch.int32)
     nr = torch.empty_like(F.rank32)
     ni = torch.empty_like(F.rank32)
-    ws = N.workspace(mesh.grid_dims, dev)
+    ws = _workspace(mesh, dev)
     rep = N.lts_pass_report_t()
     view = N.lts_regions_view_t()
     with torch.cuda.device(dev):
-        N.check(N.load().lts_remove_pass(0 if kind == "max" else 1, N.ptr(F.rank32), N.ptr(inv), N.ptr(pmark),
-                                         mesh.dim, N.dims_arg(mesh.grid_dims), int(max_iterations),
-                                         N.ptr(nr), N.ptr(ni), None, ctypes.byref(rep),
-                                         ctypes.byref(view), N.ptr(ws), ws.numel(), N.stream_ptr(dev)))
+        head = (0 if kind == "max" else 1, N.ptr(F.rank32), N.ptr(inv), N.ptr(pmark))
+        tail = (int(max_iterations), N.ptr(nr), N.ptr(ni), None, ctypes.byref(rep), ctypes.byref(view),
+                N.ptr(ws), ws.numel(), N.stream_ptr(dev))
+        if mesh.is_grid:
+            N.check(N.load().lts_remove_pass(*head, mesh.dim, N.dims_arg(mesh.grid_dims), *tail))
+        else:
+            d = mesh.device_arrays(dev)
+            N.check(N.load().lts_remove_pass_csr(*head, mesh.n, N.ptr(d["indptr"]), N.ptr(d["indices"]), *tail))
         torch.cuda.current_stream(dev).synchronize()
     R, S = int(view.regions), int(view.slots)
     pr = PassReport(kind, rep.seeds, rep.regions, rep.claimed, rep.largest, rep.n_iter_max,

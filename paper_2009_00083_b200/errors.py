@@ -7,6 +7,14 @@ class MeshError(ValueError):
     """Invalid or unsupported mesh input (reference triangulation.py:18)."""
 
 
+class NonTriangleFace(MeshError):
+    """A face with other than three vertices (reference triangulation.py:22)."""
+
+
+class NonManifoldEdge(MeshError):
+    """An edge shared by more than two triangles (reference triangulation.py:26)."""
+
+
 class FieldError(ValueError):
     """Invalid scalar-field input (reference order.py:19)."""
 

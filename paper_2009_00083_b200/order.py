@@ -148,13 +148,15 @@ class ZetaPolicy:
 def compute_order_field(f: ScalarField) -> OrderField:
     """Sort vertices by (value, id) on the device (order.py:86-91)."""
     mesh = f.mesh
-    dims = N.dims_arg(mesh.grid_dims)
     rank = torch.empty(mesh.n, dtype=torch.int32, device=f.values.device)
     inv = torch.empty(mesh.n, dtype=torch.int32, device=f.values.device)
     dev = f.values.device
-    ws = N.workspace(mesh.grid_dims, dev)
+    if mesh.is_grid:
+        ndim, dims, ws = mesh.dim, N.dims_arg(mesh.grid_dims), N.workspace(mesh.grid_dims, dev)
+    else:  # an explicit mesh: the order field only sees its n vertices
+        ndim, dims, ws = 1, N.dims_arg((mesh.n,)), N.workspace(None, dev, explicit_n=mesh.n)
     with torch.cuda.device(dev):
-        N.check(N.load().lts_order_field(N.ptr(f.values), mesh.dim, dims, N.ptr(rank), N.ptr(inv),
+        N.check(N.load().lts_order_field(N.ptr(f.values), ndim, dims, N.ptr(rank), N.ptr(inv),
                                          N.ptr(ws), ws.numel(), N.stream_ptr(dev)))
     return OrderField(rank32=rank, inverse32=inv)
 

@@ -51,6 +51,9 @@ def compute_extremum_saddle_pairs(mesh: Triangulation, f, F: Optional[OrderField
     """SPEC compute_extremum_saddle_pairs."""
     if polarity not in ("max", "min"):
         raise ValueError("polarity must be 'max' or 'min' (use both calls for 'both')")
+    if not mesh.is_grid:
+        from .errors import MeshError
+        raise MeshError("the persistence-driven mode runs on grids (explicit meshes: simplify_field)")
     if not isinstance(f, ScalarField):
         f = ScalarField(mesh, f)
     N.require_cuda()

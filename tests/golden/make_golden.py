@@ -42,6 +42,10 @@ classify_grid_serial = numba.njit(cache=False)(K.classify_grid.py_func)
 def ref_classify(mesh, rank):
     lo = np.empty(mesh.n, np.int16)
     up = np.empty(mesh.n, np.int16)
+    if not mesh.is_grid:  # explicit mesh: the reference's classify_explicit
+        K.classify_explicit(np.asarray(rank, np.int64), mesh.indptr, mesh.indices, mesh.link_ptr,
+                            mesh.link_a, mesh.link_b, lo, up)
+        return lo, up
     offs, pairs = T.grid_link_tables(mesh.dim)
     dims = np.asarray(mesh.grid_dims, np.int64)
     strides = np.array([1, dims[0]] + ([dims[0] * dims[1]] if mesh.dim == 3 else []), np.int64)
@@ -177,6 +181,8 @@ def cases():
     out.append(("cfg1_64", S.cfg1(0, N=64), 4, 1))
     out.append(("cfg2_16", S.cfg2(0, N=16), 8, 1))
     out.append(("cfg3_32", S.cfg3(0, N=32), 10, 10))
+    # scaled cfg3 whose maxima pass is non-empty (cfg3_32 has one maximum)
+    out.append(("cfg3_48_s5", S.cfg3(5, N=48), 1, 3))
     out.append(("cfg4_192", S.cfg4(0, N=192, ndisk=20), 20, 1))
     out.append(("cfg5_24", S.cfg5(0, N=24), 12, 12))
     # outer loop > 1 and capped (status 2) regions (SURVEY F5 at small scale)
@@ -202,8 +208,10 @@ def sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-def main():
+def main(only=()):
     for name, f, kmax, kmin in cases():
+        if only and name not in only:
+            continue
         dims = tuple(f.shape[::-1])
         mesh = T.build_grid_triangulation(dims)
         f32 = np.ascontiguousarray(f.ravel(), np.float32)
@@ -234,4 +242,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]))

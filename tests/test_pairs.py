@@ -130,3 +130,50 @@ def test_persistence_curve_monotone():
     assert np.all(np.diff(cnt) <= 0)
     thr, cnt = persistence_curve([], None)
     assert thr.size == 0 and cnt.size == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", GOLD, ids=IDS)
+def test_gpu_pairs_global_memory_sweep(path, monkeypatch):
+    """The Elder-rule sweep's global-memory branch (taken by fields with more
+    than ~56 K forest nodes left after peeling, e.g. cfg2 and cfg4) forced on
+    the reference fixtures: same pairs."""
+    import torch
+
+    import paper_2009_00083_b200 as P
+    monkeypatch.setenv("LTS_PAIRS_FORCE_GLOBAL", "1")
+    dims, f, eps = _case(path)
+    z = _load(path)
+    mesh = P.build_grid_triangulation(dims)
+    fd = torch.from_numpy(f).cuda()
+    for kind in ("max", "min"):
+        for i, e in enumerate(eps):
+            pr = P.compute_extremum_saddle_pairs(mesh, fd, polarity=kind, epsilon=float(e))
+            np.testing.assert_array_equal(pr.saddles.cpu().numpy(), z[f"{kind}_saddle_{i}"])
+
+
+FULL_PAIRS = os.path.join(os.path.dirname(__file__), "golden", "full_pairs.json")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", sorted(__import__("json").load(open(FULL_PAIRS))) if os.path.exists(FULL_PAIRS) else [])
+def test_gpu_pairs_full_size(key):
+    """Full-size cfg1-3 pairings (both polarities, eps = inf and 1 % of the
+    range) against the oracle's digests (tools/make_full_pairs.py); cfg2 runs
+    the global-memory sweep branch (> 56 K forest nodes)."""
+    import hashlib
+    import json
+
+    import torch
+
+    import paper_2009_00083_b200 as P
+    from paper_2009_00083_b200 import synthetic as S
+    rec = json.load(open(FULL_PAIRS))[key]
+    f = S.make_field(rec["cfg"], rec["seed"]).ravel()
+    mesh = P.build_grid_triangulation(S.CONFIGS[rec["cfg"]].dims)
+    fd = torch.from_numpy(f).cuda()
+    pr = P.compute_extremum_saddle_pairs(mesh, fd, polarity=rec["kind"], epsilon=float(rec["eps"]))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, np.int64).tobytes()).hexdigest()
+    assert int(pr.extrema.numel()) == rec["count"]
+    assert sha(pr.extrema.cpu().numpy()) == rec["extrema_sha"]
+    assert sha(pr.saddles.cpu().numpy()) == rec["saddles_sha"]
