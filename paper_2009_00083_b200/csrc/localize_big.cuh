@@ -580,8 +580,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
             S.hi_sw = max(S.hi_sw, mch >> 5);
             S.hi_chunk = max(S.hi_chunk, mch >> (BIG_CHUNK_SHIFT - 5));
           }
-          __syncwarp();
-          __threadfence_block();
+          __syncwarp();  // orders the commit's shared / global updates before the next gather
           WARP_TICK(22)
           ew += jw;
           nws++;
