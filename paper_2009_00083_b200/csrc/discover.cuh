@@ -506,19 +506,20 @@ struct BvArgs {
   uint8_t *cst, *vcls;
   unsigned long long *bestP, *best;
   int *ea, *eb, *ew;
-  int ne;
+  const int *ne;  // device: edge count written by the edge kernels (no host readback)
   int *state;
 };
 
 __global__ void __launch_bounds__(256) k_bv_coop(BvArgs a) {
   cg::grid_group grid = cg::this_grid();
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const int ne = *a.ne;
   for (int round = 0; round < 64; round++) {
     bv_reset(a.mlist, a.nm, a.best);
     if (lead) a.state[0] = 0;
     grid.sync();
     bv_pmax(a.mlist, a.nm, a.comp, a.cst, a.vcls, a.bestP, a.best);
-    if (a.ne > 0) bv_best(a.ea, a.eb, a.ew, a.ne, a.comp, a.cst, a.best);
+    if (ne > 0) bv_best(a.ea, a.eb, a.ew, ne, a.comp, a.cst, a.best);
     grid.sync();
     bv_hook(a.mlist, a.nm, a.comp, a.cst, a.best, a.par, a.wc, a.err);
     grid.sync();
@@ -559,8 +560,9 @@ __device__ __forceinline__ void uf_union(int *p, int a, int b) {
 }
 
 __global__ void k_region_union(const int *__restrict__ ea, const int *__restrict__ eb,
-                               const int *__restrict__ ew, int ne, const uint8_t *__restrict__ vcls,
-                               const int *__restrict__ acc, int *rpar) {
+                               const int *__restrict__ ew, const int *__restrict__ ne_dev,
+                               const uint8_t *__restrict__ vcls, const int *__restrict__ acc, int *rpar) {
+  const int ne = *ne_dev;
   GRID_STRIDE(i, ne) {
     int a = ea[i], b = eb[i];
     if (vcls[a] != 1 || vcls[b] != 1) continue;

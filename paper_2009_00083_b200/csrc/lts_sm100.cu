@@ -223,6 +223,7 @@ struct WS {
   rs::Bufs sb;
   int *bsum;
   int *scal;  // 64 device scalars
+  int *pstats;  // 4 per reported pass: N_I max, capped, status-1 regions, largest
   size_t bytes;
 };
 
@@ -300,6 +301,7 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->sb.nonfinite = i32(4);
   w->bsum = i32(n / SCAN_TILE + 2);
   w->scal = i32(SC_N);
+  w->pstats = i32(4 * LTS_MAX_REPORT_PASSES + 4);
   w->bytes = off + 256;
   return (int64_t)w->bytes;
 }
@@ -562,7 +564,8 @@ __global__ void k_order_keys(const int *rsize, int R, uint32_t *key) {
 // classified: w.flags / w.ptr already hold this pass's classification of rank
 static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uint8_t *pmark,
                     int max_iter, int *new_rank, int *new_inv, float *g, lts_pass_report_t *rep,
-                    lts_regions_view_t *view, bool classified = false) {
+                    lts_regions_view_t *view, bool classified = false, int *pstats = nullptr,
+                    bool list_mode = false) {
   WS &w = c.w;
   const int64_t n = c.n;
   const int ni = (int)n;
@@ -602,14 +605,20 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     g_launches += 3;
     // maxima-graph edges, de-duplicated per manifold pair in a hash table
     // sized from the maxima count; list mode if the table would overflow
-    static const bool force_list = getenv("LTS_FORCE_EDGE_LIST") != nullptr;  // test hook
+    static const bool force_list_env = getenv("LTS_FORCE_EDGE_LIST") != nullptr;  // test hook
+    const bool force_list = force_list_env || list_mode;
     int hbits = 12;
     while (hbits < 30 && (1ll << hbits) < 64ll * nm) hbits++;
     while (hbits > 10 && 18ll << hbits > 12 * w.emax) hbits--;
     EdgeHash H{(unsigned long long *)w.ebuf, (int *)(w.ebuf + (8ll << hbits)), hbits,
                w.scal + SC_ECOUNT, w.scal + SC_ACTIVE};
     int *ea = w.ea, *eb = w.eb, *ew = w.ew;
-    for (int mode = force_list ? 1 : 0; mode < 2; mode++) {
+    // One attempt (hash table, or list mode when forced): the edge count
+    // stays on the device and the table overflow flag is read back together
+    // with the Boruvka / region results below; an overflow reruns the pass in
+    // list mode (the inputs are untouched until then).
+    {
+      const int mode = force_list ? 1 : 0;
       if (mode == 0) {
         ea = (int *)(w.ebuf + (12ll << hbits));
         eb = ea + (1ll << (hbits - 1));
@@ -638,11 +647,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         g_launches++;
       }
       LTS_KCHECK();
-      LTS_TRY(readback(c, SC_ECOUNT, 2));
-      if (mode == 0 && c.h_scal[SC_ACTIVE] == 0) break;
     }
-    const int ne = c.h_scal[SC_ECOUNT];
-    r.maxima_edges = ne;
     // Boruvka rounds: tau(m) = bottleneck to preserved maxima, all rounds in
     // one cooperative launch (grid barriers between phases); one readback
     {
@@ -655,24 +660,29 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         coop_blocks = std::max(1, std::min(per, LTS_BV_COOP_PER_SM)) * nsm;
       }
       BvArgs ba{w.mlist, nm, w.comp, w.par, w.wc, w.rt, w.acc, w.scal + SC_ERR, w.cst, w.vcls, w.bestP, w.best,
-                ea, eb, ew, ne, w.scal + SC_BVSTATE};
+                ea, eb, ew, w.scal + SC_ECOUNT, w.scal + SC_BVSTATE};
       void *kargs[] = {&ba};
       LTS_CUDA(cudaLaunchCooperativeKernel((const void *)k_bv_coop, dim3(coop_blocks), dim3(256), kargs, 0, s));
       g_launches++;
       LTS_KCHECK();
-      LTS_TRY(readback(c, SC_ERR, SC_BVSTATE + 2 - SC_ERR));
-      if (c.h_scal[SC_ERR]) return lts_set_error(LTS_E_NO_SADDLE, "a discarded extremum cannot reach a preserved one");
-      r.boruvka_rounds = c.h_scal[SC_BVSTATE + 1];
     }
     // regions: union-find over edges between claimed endpoints
-    if (ne > 0) k_region_union<<<NB(ne), 256, 0, s>>>(ea, eb, ew, ne, w.vcls, w.acc, w.rpar);
+    k_region_union<<<148 * 8, 256, 0, s>>>(ea, eb, ew, w.scal + SC_ECOUNT, w.vcls, w.acc, w.rpar);
     k_region_roots<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, w.acc, rank, rev, ni, w.rpar, w.ridx,
                                            w.scal + SC_NREG, w.rsad, w.rtop, w.rsize);
     k_region_tops<<<NB(nm), 256, 0, s>>>(w.mlist, nm, w.vcls, rank, rev, ni, w.rpar, w.ridx, w.rtop);
     k_region_label<<<NB(n), 256, 0, s>>>(rank, rev, ni, w.M, w.vcls, w.acc, w.rpar, w.ridx, w.reg_of, w.rsize, w.cbits);
     g_launches += 4;
     LTS_KCHECK();
-    LTS_TRY(readback(c, SC_NREG, 1));
+    // one readback for the edge count / table overflow, Boruvka state and
+    // the region count
+    LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_BVSTATE, w.scal + SC_BVSTATE, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+    LTS_TRY(readback(c, SC_ECOUNT, SC_NREG + 1 - SC_ECOUNT));
+    if (!force_list && c.h_scal[SC_ACTIVE])  // hash table overflow: rerun in list mode
+      return run_pass(c, kind, rank, inv, pmark, max_iter, new_rank, new_inv, g, rep, view, true, pstats, true);
+    if (c.h_scal[SC_ERR]) return lts_set_error(LTS_E_NO_SADDLE, "a discarded extremum cannot reach a preserved one");
+    r.maxima_edges = c.h_scal[SC_ECOUNT];
+    r.boruvka_rounds = c.h_scal[SC_BVSTATE + 1];
     R = c.h_scal[SC_NREG];
   }
   {
@@ -689,6 +699,11 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
                                                      w.flagscan, w.scal + SC_C);
       g_launches++;
     }
+    // regions are ordered largest first: the first nbig (k > BIG_THRESHOLD) go
+    // to the CTA-batched flood on a side stream, the rest to warp floods
+    k_count_big<<<NB(R), 256, 0, s>>>(w.rsize, R, BIG_THRESHOLD, w.scal + SC_NBIG);
+    g_launches++;
+    LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_NBIG, w.scal + SC_NBIG, sizeof(int) * 8, cudaMemcpyDeviceToHost, s));
     LTS_TRY(readback(c, SC_S, 2));
     S = c.h_scal[SC_S];
     C = c.h_scal[SC_C];
@@ -709,11 +724,6 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     A.verts = w.verts; A.reg_of = w.reg_of; A.loc_of = w.loc_of; A.buf0 = w.buf0; A.buf1 = w.buf1;
     A.buf2 = w.buf2; A.out = w.out; A.gheap = w.gheap; A.sfl = w.sfl; A.n_iters = w.nit;
     A.status = w.st; A.max_iter = max_iter; A.queue = w.scal + SC_QUEUE; A.qbase = 0;
-    // regions are ordered largest first: the first nbig (k > BIG_THRESHOLD) go
-    // to the CTA-batched flood on a side stream, the rest to warp floods
-    k_count_big<<<NB(R), 256, 0, s>>>(w.rsize, R, BIG_THRESHOLD, w.scal + SC_NBIG);
-    g_launches++;
-    LTS_TRY(readback(c, SC_NBIG, 8));
     const int nbig = c.h_scal[SC_NBIG];
     r.big_regions = nbig;
     BigArgs B{};
@@ -790,14 +800,18 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       g_launches++;
       LTS_TRY(big_stream_join(s));
     }
-    k_loc_stats<<<NB(R), 256, 0, s>>>(w.nit, w.st, w.rsize, R, w.scal + SC_STATS);
+    // per-pass N_I / capped / status-1 / largest: into the caller's device
+    // slots (read back once at the end of lts_simplify), else read now
+    k_loc_stats<<<NB(R), 256, 0, s>>>(w.nit, w.st, w.rsize, R, pstats ? pstats : w.scal + SC_STATS);
     g_launches += 1;
     LTS_KCHECK();
-    LTS_TRY(readback(c, SC_STATS, 4));
-    r.n_iter_max = c.h_scal[SC_STATS];
-    r.capped = c.h_scal[SC_STATS + 1];
-    r.largest = c.h_scal[SC_STATS + 3];
-    if (c.h_scal[SC_STATS + 2]) return lts_set_error(LTS_E_LOCALIZE_NO_MIN, "region without an admissible boundary minimum (status 1)");
+    if (!pstats) {
+      LTS_TRY(readback(c, SC_STATS, 4));
+      r.n_iter_max = c.h_scal[SC_STATS];
+      r.capped = c.h_scal[SC_STATS + 1];
+      r.largest = c.h_scal[SC_STATS + 3];
+      if (c.h_scal[SC_STATS + 2]) return lts_set_error(LTS_E_LOCALIZE_NO_MIN, "region without an admissible boundary minimum (status 1)");
+    }
   }
   {
     Phase ph(c, LTS_PH_INTEGRATE);
@@ -894,7 +908,7 @@ int64_t lts_kernel_launches(void) { return g_launches; }
 // ---------------------------------------------------------------------------
 // persistence-driven mode: extremum-saddle pairs (persistence.cuh)
 // ---------------------------------------------------------------------------
-static int order_field_impl(Ctx &c, const float *f, int32_t *rank, int32_t *inverse);
+static int order_field_impl(Ctx &c, const float *f, int32_t *rank, int32_t *inverse, bool defer_check = false);
 
 static int pairs_impl(Ctx &c, const float *f, const int *rank, const int *inv, int kind, double eps,
                       int32_t *ext_out, int32_t *sad_out, int64_t *count_out) {
@@ -1143,13 +1157,16 @@ int lts_workspace_size(int ndim, const int64_t *dims, size_t *bytes) {
   return 0;
 }
 
-static int order_field_impl(Ctx &c, const float *f, int32_t *rank, int32_t *inverse) {
+// defer_check: the caller reads w.sb.nonfinite back later (with its own
+// readback) instead of synchronising here
+static int order_field_impl(Ctx &c, const float *f, int32_t *rank, int32_t *inverse, bool defer_check) {
   WS &w = c.w;
   Phase ph(c, LTS_PH_ORDER);
   LTS_CUDA(cudaMemsetAsync(w.sb.nonfinite, 0, sizeof(int), c.s));
   uint32_t *inv_out = inverse ? (uint32_t *)inverse : w.sval;
   LTS_TRY(radix_sort((const uint32_t *)f, nullptr, c.n, 32, true, nullptr, inv_out, rank, w.sb, c.s));
   LTS_KCHECK();
+  if (defer_check) return 0;
   LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_TMP, w.sb.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, c.s));
   LTS_CUDA(cudaStreamSynchronize(c.s));
   if (c.h_scal[SC_TMP]) return lts_set_error(LTS_E_FIELD_NONFINITE, "scalar field contains NaN or infinite values");
@@ -1246,7 +1263,7 @@ static int simplify_impl(Ctx &c, const float *f, const int64_t *pres_max, int64_
   if (order) {
     LTS_TRY(install_order(c, f, order));
   } else {
-    LTS_TRY(order_field_impl(c, f, w.rankA, w.invA));
+    LTS_TRY(order_field_impl(c, f, w.rankA, w.invA, true));
   }
   // preserve marks and validation
   LTS_CUDA(cudaMemsetAsync(w.pmark, 0, (size_t)n, s));
@@ -1264,17 +1281,23 @@ static int simplify_impl(Ctx &c, const float *f, const int64_t *pres_max, int64_
   if (g) k_copy_canon<<<NB(n), 256, 0, s>>>(f, g, n);
   g_launches += g ? 4 : 3;
   LTS_KCHECK();
+  // one readback: the order field's finiteness flag and the preserve check
+  c.h_scal[SC_TMP] = 0;
+  if (!order) LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_TMP, w.sb.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, s));
   LTS_TRY(readback(c, SC_BADPRES, 1));
+  if (c.h_scal[SC_TMP]) return lts_set_error(LTS_E_FIELD_NONFINITE, "scalar field contains NaN or infinite values");
   if (c.h_scal[SC_BADPRES]) return lts_set_error(LTS_E_CONSTRAINT_NOT_EXTREMUM, "a preserved vertex is not an extremum of the input order (ConstraintNotExtremum)");
 
   int *cr = w.rankA, *ci = w.invA, *nr = w.rankB, *ni = w.invB;
   bool ok = false;
   int it = 0;
+  LTS_CUDA(cudaMemsetAsync(w.pstats, 0, sizeof(int) * (4 * LTS_MAX_REPORT_PASSES + 4), s));
   for (it = 1; it <= o.max_iterations; it++) {
     for (int kind = 0; kind < 2; kind++) {
       lts_pass_report_t pr{};
+      const int slot = std::min(R.n_passes, LTS_MAX_REPORT_PASSES);  // the last slot collects the overflow
       LTS_TRY(run_pass(c, kind, cr, ci, w.pmark, o.max_iterations, nr, ni, g, &pr, nullptr,
-                       it == 1 && kind == 0));
+                       it == 1 && kind == 0, w.pstats + 4 * slot));
       if (R.n_passes < LTS_MAX_REPORT_PASSES) R.passes[R.n_passes++] = pr;
       if (o.region_ni_out && pr.regions > 0) {  // per-region N_I
         const int64_t room = o.region_ni_capacity - R.region_ni_count;
@@ -1342,7 +1365,19 @@ static int simplify_impl(Ctx &c, const float *f, const int64_t *pres_max, int64_
     t1 = next_event();
     cudaEventRecord(t1, s);
   }
+  std::vector<int> pst(4 * LTS_MAX_REPORT_PASSES + 4);
+  LTS_CUDA(cudaMemcpyAsync(pst.data(), w.pstats, sizeof(int) * pst.size(), cudaMemcpyDeviceToHost, s));
   LTS_CUDA(cudaStreamSynchronize(s));
+  bool status1 = false;
+  for (int i = 0; i < R.n_passes; i++) {
+    if (R.passes[i].regions == 0) continue;
+    const int *q = pst.data() + 4 * i;
+    R.passes[i].n_iter_max = q[0];
+    R.passes[i].capped = q[1];
+    R.passes[i].largest = q[3];
+    status1 |= q[2] != 0;
+  }
+  if (status1) return lts_set_error(LTS_E_LOCALIZE_NO_MIN, "region without an admissible boundary minimum (status 1)");
   if (c.timing) {
     for (auto &m : c.marks) {
       float ms = 0;
