@@ -334,6 +334,9 @@ __device__ int big_warp_gather(BigSmem &S, int &key) {
   return nc;
 }
 
+#ifndef LTS_BIG_HW_FROM_BLOCK
+#define LTS_BIG_HW_FROM_BLOCK 1
+#endif
 #ifndef LTS_BIG_WARP_ENTER
 #define LTS_BIG_WARP_ENTER 24  // a block step committing fewer keys enters warp mode
 #endif
@@ -608,6 +611,11 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     const int nc = big_gather(S, S.hi_chunk, leaf4, key);
     BIG_TICK(8)
     if (nc == 0) break;
+    // the top frontier word bounds the warp gather's start (the commit below
+    // raises it for higher exposures, after the cut's barriers)
+#if LTS_BIG_HW_FROM_BLOCK
+    if (tid == 0) S.hw = key >> 5;
+#endif
     const bool isc = tid < nc;
     int cand_p = 0;
     if (isc) {
@@ -681,7 +689,7 @@ __device__ void big_flood(BigSmem &S, BigRegion &G, bool asc, const int *cin, in
     }
     if (tid == 0) {
       S.cutbuf[par ^ 1] = 0x7fffffff;
-      if (j < LTS_BIG_WARP_ENTER) S.wmode = 1;
+      if (j < LTS_BIG_WARP_ENTER) S.wmode = 1;  // few keys committed: warp mode
     }
     par ^= 1;
     __syncthreads();
