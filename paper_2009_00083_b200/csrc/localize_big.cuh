@@ -74,7 +74,9 @@ __device__ __forceinline__ int big_locate(const BigArgs &Bg, int i) {
 
 // per-region flood state, kept in global memory between the grid-wide
 // setup / check kernels and the one-CTA-per-region flood kernel
-enum { BST_T = 0, BST_ACTIVE, BST_FIN, BST_STATUS, BST_BAD, BST_DIFF, BST_W = 8 };
+// BST_NSRC: sources of the coming ascending flood; BST_LEVEL: the region floods
+// level-parallel (localize_level.cuh) instead of in k_big_flood
+enum { BST_T = 0, BST_ACTIVE, BST_FIN, BST_STATUS, BST_BAD, BST_DIFF, BST_NSRC, BST_LEVEL, BST_W = 8 };
 
 // optional per-region instrumentation (lts_debug_big_stats): big-queue slot i
 // records [k, frontier steps, candidates, committed, flood cycles, global-rule
@@ -807,7 +809,7 @@ __device__ __forceinline__ BigRef big_ref(const LocArgs &A, const BigArgs &Bg, i
 }
 
 // per region: v0 from k_big_rows; no admissible minimum -> status 1
-__global__ void k_big_init(LocArgs A, BigArgs Bg) {
+__global__ void k_big_init(LocArgs A, BigArgs Bg, int level_min) {
   GRID_STRIDE(qi, Bg.nbig) {
     const BigRef R = big_ref(A, Bg, (int)qi);
     const int v0 = Bg.v0[qi];
@@ -815,6 +817,8 @@ __global__ void k_big_init(LocArgs A, BigArgs Bg) {
     st[BST_T] = 0;
     st[BST_BAD] = 0;
     st[BST_DIFF] = 0;
+    st[BST_NSRC] = 0;
+    st[BST_LEVEL] = level_min >= 0 && R.k >= level_min ? 1 : 0;
     if (v0 == 0x7fffffff) {
       st[BST_ACTIVE] = 0;
       st[BST_FIN] = -1;
@@ -874,7 +878,7 @@ __global__ void __launch_bounds__(BIG_T) k_big_flood(LocArgs A, BigArgs Bg) {
   const int tid = threadIdx.x;
   const int qi = blockIdx.x;
   int *st = Bg.st + qi * BST_W;
-  if (!st[BST_ACTIVE]) return;
+  if (!st[BST_ACTIVE] || st[BST_LEVEL]) return;
   const int t = st[BST_T];
   BigRegion G;
   G.rid = A.order[Bg.qbase + qi];
@@ -987,6 +991,7 @@ __global__ void k_big_decide(LocArgs A, BigArgs Bg) {
     const bool bad = st[BST_BAD] != 0, diff = st[BST_DIFF] != 0;
     st[BST_BAD] = 0;
     st[BST_DIFF] = 0;
+    st[BST_NSRC] = 0;
     bool done = true;
     if (!bad) {
       st[BST_FIN] = t;

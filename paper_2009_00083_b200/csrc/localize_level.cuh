@@ -1,0 +1,369 @@
+// localize_level.cuh -- exact priority floods of large regions by level-parallel
+// decomposition (no sequential extraction loop).
+//
+// A max-first priority flood from a source b over a vertex set C with distinct
+// keys (_kernels.py:491-552) factors exactly:
+//   * let beta(v) be the vertex of smallest key on the maximin (bottleneck)
+//     path from b to v inside C (b itself excluded; b counts as +infinity);
+//   * the "trunk" {t : beta(t) = t} is the sequence of record lows of the
+//     flood; the classes {v : beta(v) = t} are extracted contiguously, in
+//     decreasing key(t), each one starting with t;
+//   * inside a class the order is the same flood started at t, with t's own
+//     adjacency and t counted as +infinity.
+// So the extraction order is the preorder of a forest F (parent of v = the
+// trunk vertex of the level at which v became a trunk vertex's class member,
+// i.e. the source of the flood task in which v is a record low) with children
+// visited in decreasing key, and the subtree sizes of F are the class sizes.
+// Bottleneck paths are paths of a maximum spanning tree under the edge weight
+// min(key u, key v), so one level is data-parallel over all tasks of all
+// regions at once:
+//   1. Boruvka maximum spanning forest of every task's member graph, kept
+//      rooted at the task's source (a hooking component reverses the path from
+//      its hook vertex to its old root); the source's component never hooks;
+//   2. beta by pointer jumping (argmin of the key along the root path);
+//   3. class sizes, new tasks (source beta(v)) for the vertices off the trunk.
+// Levels repeat until every vertex is a trunk vertex of some level; a final
+// stable sort by F-parent, a segmented prefix of the class sizes and pointer
+// jumping over F give every vertex its extraction index.  Ascending floods
+// (many sources, min-first) are the same flood on reversed keys from a virtual
+// root adjacent to every source.  The decomposition was checked against heap
+// floods of the reference on the regions of the BASELINE configs (2-D and 3-D,
+// single and multi source) and is covered bit-exactly by the parity tests.
+//
+// Everything is indexed in "key space": j = jb(region) + key, keys in [0, k],
+// jb = bpre[qi] + qi; within a region j is monotone in the key, so keys are
+// compared through j.  The neighbour keys of every key come from k_big_setup
+// (BigArgs::nrowkey), as for the CTA floods.
+#pragma once
+#include "localize_big.cuh"
+
+namespace lts {
+
+constexpr int LV_DONE = -1;
+constexpr unsigned LV_NONE = 0xffffffffu;
+enum { LVC_HOOKS = 0, LVC_CHANGED = 1, LVC_ACTIVE = 2, LVC_ERR = 3, LVC_N = 8 };
+
+struct LvArgs {
+  int *task;    // j: source (j index) of the flood task the vertex belongs to, LV_DONE when placed
+  unsigned *fp; // j: F-parent (j index), LV_NONE for sources / non-vertices
+  int *par;     // j: parent in the rooted spanning forest
+  int *comp;    // j: component label (= j of the component's tree root) at round start
+  int *link;    // labels: hook target of this round
+  int *csize;   // j: class size (F-subtree size) of a trunk vertex
+  int *off;     // j: level-1 source mark during the flood
+  int *skey, *sval, *oval;  // final sort / scan buffers
+  unsigned long long *best;  // labels: best outgoing edge (min j, max j | INF)
+  unsigned long long *pm;    // j: (value, ancestor) pairs of the two pointer-jumping phases
+  int *ctr;
+  int nj;
+  int level;
+};
+
+struct LvRef {
+  int qi, rid, lo, k, jb, t;
+  bool active, asc;
+};
+
+__device__ __forceinline__ LvRef lv_ref(const LocArgs &A, const BigArgs &Bg, int j) {
+  int lo = 0, hi = Bg.nbig - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (Bg.bpre[mid] + mid <= j) lo = mid;
+    else hi = mid - 1;
+  }
+  LvRef R;
+  R.qi = lo;
+  R.jb = Bg.bpre[lo] + lo;
+  R.rid = A.order[Bg.qbase + lo];
+  R.lo = A.rptr[R.rid];
+  R.k = A.rptr[R.rid + 1] - R.lo;
+  const int *st = Bg.st + lo * BST_W;
+  R.t = st[BST_T];
+  R.active = st[BST_ACTIVE] != 0 && st[BST_LEVEL] != 0;
+  R.asc = R.t & 1;
+  return R;
+}
+
+__device__ __forceinline__ unsigned long long lv_pack(unsigned hi, unsigned lo) {
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+// sources of the coming ascending flood, per region (flat over big-region slots)
+__global__ void __launch_bounds__(256) k_lv_nsrc(LocArgs A, BigArgs Bg) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Bg.bslots; i += gridDim.x * blockDim.x) {
+    const int qi = big_locate(Bg, i);
+    int *st = Bg.st + qi * BST_W;
+    if (!st[BST_ACTIVE] || !st[BST_LEVEL] || !(st[BST_T] & 1)) continue;
+    const BigRef R = big_ref(A, Bg, qi);
+    const int p = i - Bg.bpre[qi];
+    if (p >= 1 && (A.sfl[R.lo + p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) atomicAdd(st + BST_NSRC, 1);
+  }
+}
+
+// tasks of level 1: every vertex of a flooding region belongs to the task of
+// the region's source (desc) or virtual root (asc, at the unused key k)
+__global__ void __launch_bounds__(256) k_lv_init(LocArgs A, BigArgs Bg, LvArgs L) {
+  int mine = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+    L.task[j] = LV_DONE;
+    L.fp[j] = LV_NONE;
+    L.off[j] = 0;
+    L.csize[j] = 0;
+    const LvRef R = lv_ref(A, Bg, j);
+    if (!R.active) continue;
+    const int kap = j - R.jb;
+    const int *cin = big_buf(A, R.t) + R.lo;
+    if (R.asc) {
+      if (Bg.st[R.qi * BST_W + BST_NSRC] == 0) continue;  // empty ascending flood: labels kept
+      if (kap == R.k) continue;                           // the virtual root
+      const int p = Bg.inv[R.lo + R.rid + kap];
+      L.task[j] = R.jb + R.k;
+      if (p >= 1 && (A.sfl[R.lo + p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) L.off[j] = 1;
+      mine++;
+    } else {
+      const int unused = R.t == 0 ? Bg.v0[R.qi] : R.k;
+      const int src = flood_key(cin[0], false, R.k);
+      if (kap == unused || kap == src) continue;
+      L.task[j] = R.jb + src;
+      mine++;
+    }
+  }
+  mine = __reduce_add_sync(0xffffffffu, mine);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(L.ctr + LVC_ACTIVE, mine);
+}
+
+// per level: singleton components, no tree edges; the level-1 sources of an
+// ascending flood start inside the root's component
+__global__ void __launch_bounds__(256) k_lv_prep(LvArgs L) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+    const int tk = L.task[j];
+    if (tk < 0) continue;
+    int c = j, p = -1;
+    if (L.level == 1 && L.off[j] == 1) c = p = tk;
+    L.comp[j] = c;
+    L.link[j] = j;
+    L.par[j] = p;
+    L.best[j] = 0ull;
+    L.csize[j] = 0;
+    L.comp[tk] = tk;
+    L.link[tk] = tk;
+  }
+}
+
+// Boruvka round, step 1: every vertex outside its task's root component offers
+// its heaviest edge leaving its component (weight: (min j, max j), the root
+// counting as +infinity) to the component's label
+template <int K>
+__global__ void __launch_bounds__(256) k_lv_scan(LocArgs A, BigArgs Bg, LvArgs L) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+    const int tk = L.task[j];
+    if (tk < 0) continue;
+    const int c = L.comp[j];
+    if (c == tk) continue;
+    const LvRef R = lv_ref(A, Bg, j);
+    const int2 *row = reinterpret_cast<const int2 *>(Bg.nrowkey + ((size_t)R.lo + R.rid + (j - R.jb)) * K);
+    int q[K];
+#pragma unroll
+    for (int h = 0; h < K / 2; h++) {
+      const int2 v = row[h];
+      q[2 * h] = v.x;
+      q[2 * h + 1] = v.y;
+    }
+    unsigned long long b = 0ull;
+#pragma unroll
+    for (int kk = 0; kk < K; kk++) {
+      if (q[kk] < 0) continue;
+      const int u = R.jb + q[kk];
+      unsigned long long w;
+      if (u == tk) {
+        w = lv_pack((unsigned)j, LV_NONE);
+      } else {
+        if (L.task[u] != tk) continue;
+        if (L.comp[u] == c) continue;
+        w = lv_pack((unsigned)min(u, j), (unsigned)max(u, j));
+      }
+      b = max(b, w);
+    }
+    if (b) atomicMax(L.best + c, b);
+  }
+}
+
+// step 2: every component outside the root's hooks along its best edge: the
+// tree path from the hook vertex to the old root is reversed, so the merged
+// tree stays rooted at the target's root.  Two components choosing the same
+// edge: the larger label hooks.
+__global__ void __launch_bounds__(256) k_lv_hook(LvArgs L) {
+  int hooks = 0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.nj; c += gridDim.x * blockDim.x) {
+    const int tk = L.task[c];
+    if (tk < 0 || L.comp[c] != c) continue;
+    const unsigned long long e = L.best[c];
+    if (e == 0ull) continue;
+    const int x = (int)(e >> 32);
+    const unsigned hi = (unsigned)(e & 0xffffffffu);
+    const int y = hi == LV_NONE ? tk : (int)hi;
+    const int cx = L.comp[x];
+    const int cy = y == tk ? tk : L.comp[y];
+    int a, b, c2;
+    if (cx == c) {
+      a = x; b = y; c2 = cy;
+    } else {
+      a = y; b = x; c2 = cx;
+    }
+    if (c2 != tk && c < c2 && L.best[c2] == e) continue;
+    int prev = b, cur = a;
+    while (cur >= 0) {
+      const int nxt = L.par[cur];
+      L.par[cur] = prev;
+      prev = cur;
+      cur = nxt;
+    }
+    L.link[c] = c2;
+    hooks++;
+  }
+  hooks = __reduce_add_sync(0xffffffffu, hooks);
+  if ((threadIdx.x & 31) == 0 && hooks) atomicAdd(L.ctr + LVC_HOOKS, hooks);
+}
+
+// step 3: labels of the merged components (the label is the tree root)
+__global__ void __launch_bounds__(256) k_lv_jump(LvArgs L) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+    if (L.task[j] < 0) continue;
+    const int c = L.comp[j];
+    int r = c, nx;
+    while ((nx = L.link[r]) != r) r = nx;
+    int cur = c;
+    while (cur != r) {  // shorten the chain for the threads that follow
+      nx = L.link[cur];
+      if (nx != r) L.link[cur] = r;
+      cur = nx;
+    }
+    L.comp[j] = r;
+    L.best[j] = 0ull;
+  }
+}
+
+// beta: (smallest j on the tree path so far, ancestor reached)
+__global__ void __launch_bounds__(256) k_lv_pm_init(LvArgs L) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+    if (L.task[j] < 0) continue;
+    L.pm[j] = lv_pack((unsigned)j, (unsigned)L.par[j]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lv_pm_round(LvArgs L) {
+  int ch = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+    const int tk = L.task[j];
+    if (tk < 0) continue;
+    const unsigned long long a = L.pm[j];
+    const int anc = (int)(unsigned)(a & 0xffffffffu);
+    if (anc == tk) continue;
+    const unsigned long long b = L.pm[anc];
+    const unsigned m = min((unsigned)(a >> 32), (unsigned)(b >> 32));
+    L.pm[j] = lv_pack(m, (unsigned)(b & 0xffffffffu));
+    ch = 1;
+  }
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) L.ctr[LVC_CHANGED] = 1;
+}
+
+// classes of this level: trunk vertices are placed (F-parent = task source),
+// the others join the task of their class's trunk vertex
+__global__ void __launch_bounds__(256) k_lv_classes(LvArgs L) {
+  int act = 0;
+  for (int j0 = blockIdx.x * blockDim.x; j0 < L.nj; j0 += gridDim.x * blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    const int tk = j < L.nj ? L.task[j] : -1;
+    int beta = -1;
+    if (tk >= 0) {
+      beta = (int)(L.pm[j] >> 32);
+      if (beta == j) {
+        L.fp[j] = (unsigned)tk;
+        L.task[j] = LV_DONE;
+      } else {
+        L.task[j] = beta;
+        act++;
+      }
+    }
+    // one atomic per class and warp
+    const unsigned peers = __match_any_sync(0xffffffffu, beta);
+    if (beta >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(L.csize + beta, __popc(peers));
+  }
+  act = __reduce_add_sync(0xffffffffu, act);
+  if ((threadIdx.x & 31) == 0 && act) atomicAdd(L.ctr + LVC_ACTIVE, act);
+}
+
+// ---- extraction indices: preorder of F, children in decreasing key ----------
+__global__ void __launch_bounds__(256) k_lv_sortkeys(LvArgs L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.nj; i += gridDim.x * blockDim.x) {
+    const int j = L.nj - 1 - i;
+    const unsigned f = L.fp[j];
+    L.skey[i] = f == LV_NONE ? L.nj : (int)f;
+    L.sval[i] = j;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lv_gather(LvArgs L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.nj; i += gridDim.x * blockDim.x) {
+    const int j = L.oval[i];
+    L.skey[i] = L.fp[j] == LV_NONE ? 0 : L.csize[j];
+  }
+}
+
+// cum = exclusive prefix of the class sizes in sorted order (in sval); the
+// first child of every parent records the parent's base
+__global__ void __launch_bounds__(256) k_lv_heads(LvArgs L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.nj; i += gridDim.x * blockDim.x) {
+    const unsigned f = L.fp[L.oval[i]];
+    if (f == LV_NONE) continue;
+    if (i == 0 || L.fp[L.oval[i - 1]] != f) L.par[f] = L.sval[i];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lv_off(LocArgs A, BigArgs Bg, LvArgs L) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.nj; i += gridDim.x * blockDim.x) {
+    const int j = L.oval[i];
+    const unsigned f = L.fp[j];
+    if (f == LV_NONE) continue;
+    int acc = L.sval[i] - L.par[f] + 1;
+    if (L.fp[f] == LV_NONE && lv_ref(A, Bg, j).asc) acc--;  // children of the virtual root start at 0
+    L.pm[j] = lv_pack((unsigned)acc, f);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lv_pos_round(LvArgs L) {
+  int ch = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+    if (L.fp[j] == LV_NONE) continue;
+    const unsigned long long a = L.pm[j];
+    const unsigned anc = (unsigned)(a & 0xffffffffu);
+    if (L.fp[anc] == LV_NONE) continue;
+    const unsigned long long b = L.pm[anc];
+    L.pm[j] = lv_pack((unsigned)(a >> 32) + (unsigned)(b >> 32), (unsigned)(b & 0xffffffffu));
+    ch = 1;
+  }
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) L.ctr[LVC_CHANGED] = 1;
+}
+
+// state t+1 of every level-flooded region
+__global__ void __launch_bounds__(256) k_lv_write(LocArgs A, BigArgs Bg, LvArgs L) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+    const LvRef R = lv_ref(A, Bg, j);
+    if (!R.active) continue;
+    const int kap = j - R.jb;
+    const int unused = R.t == 0 ? Bg.v0[R.qi] : R.k;
+    if (kap == unused) continue;
+    const int p = Bg.inv[R.lo + R.rid + kap];
+    const int *cin = big_buf(A, R.t) + R.lo;
+    int *cout = big_buf(A, R.t + 1) + R.lo;
+    if (R.asc && Bg.st[R.qi * BST_W + BST_NSRC] == 0) {
+      cout[p] = cin[p];
+      continue;
+    }
+    const int e = L.fp[j] == LV_NONE ? 0 : (int)(L.pm[j] >> 32);
+    cout[p] = R.asc ? e : R.k - 1 - e;
+    if (p == 0) atomicAdd(Bg.work, (unsigned long long)R.k);
+  }
+}
+
+}  // namespace lts

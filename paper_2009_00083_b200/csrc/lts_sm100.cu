@@ -26,6 +26,7 @@
 #include "discover.cuh"
 #include "localize.cuh"
 #include "localize_big.cuh"
+#include "localize_level.cuh"
 #include "integrate.cuh"
 #include "persistence.cuh"
 #include "csr.cuh"
@@ -222,6 +223,10 @@ struct WS {
   uint32_t *gbits;
   rs::Bufs sb;
   int *bsum;
+  // level-parallel floods (localize_level.cuh): key-space arrays and their own sort / scan scratch
+  LvArgs lv;
+  rs::Bufs lsb;
+  int *lbsum;
   int *scal;  // 64 device scalars
   int *pstats;  // 4 per reported pass: N_I max, capped, status-1 regions, largest
   size_t bytes;
@@ -250,6 +255,8 @@ enum {
   SC_BIGWORK = 34,  // 2 ints: 64-bit sum of region sizes flooded by k_big_flood
   SC_BIGSLOTS = 36, // = SC_NBIG + 7: slots of the big regions
   SC_BVSTATE = 40,  // 2: active roots of the last Boruvka round, rounds run
+  SC_LV = 44,       // LVC_N counters of the level-parallel floods
+  SC_LVTMP = 52,
   SC_N = 64
 };
 
@@ -300,6 +307,22 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->sb.ctr = u32(8);
   w->sb.nonfinite = i32(4);
   w->bsum = i32(n / SCAN_TILE + 2);
+  {
+    // key space of the large regions: one entry per slot plus one per region
+    const int64_t nj = s2 + n1 / BIG_THRESHOLD + 8;
+    w->lv.task = i32(nj); w->lv.fp = u32(nj); w->lv.par = i32(nj); w->lv.comp = i32(nj); w->lv.link = i32(nj);
+    w->lv.csize = i32(nj); w->lv.off = i32(nj); w->lv.skey = i32(nj); w->lv.sval = i32(nj); w->lv.oval = i32(nj);
+    w->lv.best = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)nj);
+    w->lv.pm = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)nj);
+    // the final sort runs after the levels: its ping-pong buffers reuse the Boruvka arrays
+    w->lsb.k1 = (uint32_t *)w->lv.comp; w->lsb.v1 = (uint32_t *)w->lv.link;
+    w->lsb.k2 = (uint32_t *)w->lv.best; w->lsb.v2 = w->lsb.k2 ? w->lsb.k2 + nj : nullptr;
+    w->lsb.status = u32(rs::status_elems(nj));
+    w->lsb.hist = u32(4 * 256);
+    w->lsb.ctr = u32(8);
+    w->lsb.nonfinite = i32(4);
+    w->lbsum = i32(nj / SCAN_TILE + 2);
+  }
   w->scal = i32(SC_N);
   w->pstats = i32(4 * LTS_MAX_REPORT_PASSES + 4);
   w->bytes = off + 256;
@@ -527,6 +550,9 @@ static int big_stream_join(cudaStream_t s) {
 
 // one flood of every large region still flooding: grid-wide relabelling,
 // one CTA per region for the flood, grid-wide checks, per-region decision
+static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B);
+static int g_level_min = -1;  // regions of at least this many slots flood level-parallel (-1: none)
+
 static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
   const int rg = gx;
   LTS_CUDA(cudaMemsetAsync(B.nactive, 0, sizeof(int), g_bigs));
@@ -542,6 +568,7 @@ static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
   if (c.g.ndim == 2) k_big_flood<2><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
   else if (c.g.ndim == 3) k_big_flood<3><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
   else k_big_flood<0><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+  if (g_level_min >= 0) LTS_TRY(big_level_flood(c, A, B));
   if (c.timing) {
     fb = next_event();
     LTS_CUDA(cudaEventRecord(fb, g_bigs));
@@ -553,6 +580,95 @@ static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
   else k_big_check<0><<<rg, 256, 0, g_bigs>>>(A, B);
   k_big_decide<<<NB(B.nbig), 256, 0, g_bigs>>>(A, B);
   g_launches += 4;
+  LTS_KCHECK();
+  return 0;
+}
+
+// Level-parallel flood t -> t+1 of every large region flagged BST_LEVEL
+// (localize_level.cuh), between k_big_setup and k_big_check.  The host drives
+// the level / Boruvka-round / pointer-jumping loops from three counters read
+// back on the flood stream.
+static int lv_read(Ctx &c, int first, int count) {
+  LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_LV + first, c.w.scal + SC_LV + first, sizeof(int) * count,
+                           cudaMemcpyDeviceToHost, g_bigs));
+  LTS_CUDA(cudaStreamSynchronize(g_bigs));
+  return 0;
+}
+
+static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
+  WS &w = c.w;
+  LvArgs L = w.lv;
+  L.ctr = w.scal + SC_LV;
+  L.nj = B.bslots + B.nbig;
+  L.level = 0;
+  cudaStream_t s = g_bigs;
+  const int gj = (int)std::min<int64_t>(((int64_t)L.nj + 255) / 256, 148 * 8);
+  const int gs = (int)std::min<int64_t>(((int64_t)B.bslots + 255) / 256, 148 * 8);
+  int *hc = c.h_scal + SC_LV;
+  LTS_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(int) * LVC_N, s));
+  k_lv_nsrc<<<gs, 256, 0, s>>>(A, B);
+  k_lv_init<<<gj, 256, 0, s>>>(A, B, L);
+  g_launches += 2;
+  LTS_TRY(lv_read(c, LVC_ACTIVE, 1));
+  int active = hc[LVC_ACTIVE];
+  int levels = 0, rounds_total = 0;
+  while (active > 0) {
+    L.level = ++levels;
+    k_lv_prep<<<gj, 256, 0, s>>>(L);
+    g_launches++;
+    for (int round = 0;; round++) {
+      if (round >= 64) return lts_set_error(LTS_E_CUDA, "level flood: spanning forest did not converge");
+      LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_HOOKS, 0, sizeof(int), s));
+      if (c.g.ndim == 2) k_lv_scan<6><<<gj, 256, 0, s>>>(A, B, L);
+      else if (c.g.ndim == 3) k_lv_scan<14><<<gj, 256, 0, s>>>(A, B, L);
+      else k_lv_scan<kCsrK><<<gj, 256, 0, s>>>(A, B, L);
+      k_lv_hook<<<gj, 256, 0, s>>>(L);
+      k_lv_jump<<<gj, 256, 0, s>>>(L);
+      g_launches += 3;
+      rounds_total++;
+      LTS_TRY(lv_read(c, LVC_HOOKS, 1));
+      if (hc[LVC_HOOKS] == 0) break;
+    }
+    k_lv_pm_init<<<gj, 256, 0, s>>>(L);
+    g_launches++;
+    for (int it = 0;; it++) {
+      if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: path minima did not converge");
+      LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
+      k_lv_pm_round<<<gj, 256, 0, s>>>(L);
+      k_lv_pm_round<<<gj, 256, 0, s>>>(L);
+      g_launches += 2;
+      LTS_TRY(lv_read(c, LVC_CHANGED, 1));
+      if (hc[LVC_CHANGED] == 0) break;
+    }
+    LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_ACTIVE, 0, sizeof(int), s));
+    k_lv_classes<<<gj, 256, 0, s>>>(L);
+    g_launches++;
+    LTS_TRY(lv_read(c, LVC_ACTIVE, 1));
+    if (hc[LVC_ACTIVE] >= active) return lts_set_error(LTS_E_CUDA, "level flood: no progress");
+    active = hc[LVC_ACTIVE];
+  }
+  // extraction index = preorder of F, children in decreasing key
+  k_lv_sortkeys<<<gj, 256, 0, s>>>(L);
+  LTS_TRY(radix_sort((const uint32_t *)L.skey, (const uint32_t *)L.sval, L.nj, bits_for(L.nj), false, nullptr,
+                     (uint32_t *)L.oval, nullptr, w.lsb, s));
+  k_lv_gather<<<gj, 256, 0, s>>>(L);
+  LTS_TRY(scan_int(L.skey, L.sval, L.nj, w.lbsum, w.scal + SC_LVTMP, false, s));
+  k_lv_heads<<<gj, 256, 0, s>>>(L);
+  k_lv_off<<<gj, 256, 0, s>>>(A, B, L);
+  g_launches += 4;
+  for (int it = 0;; it++) {
+    if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: positions did not converge");
+    LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
+    k_lv_pos_round<<<gj, 256, 0, s>>>(L);
+    k_lv_pos_round<<<gj, 256, 0, s>>>(L);
+    g_launches += 2;
+    LTS_TRY(lv_read(c, LVC_CHANGED, 1));
+    if (hc[LVC_CHANGED] == 0) break;
+  }
+  k_lv_write<<<gj, 256, 0, s>>>(A, B, L);
+  g_launches++;
+  static const bool verbose = getenv("LTS_LEVEL_VERBOSE") != nullptr;
+  if (verbose) fprintf(stderr, "[lts] level flood: nj %d levels %d boruvka rounds %d\n", L.nj, levels, rounds_total);
   LTS_KCHECK();
   return 0;
 }
@@ -745,9 +861,16 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       if (c.g.ndim == 2) k_big_rows<2><<<big_gx, 256, 0, g_bigs>>>(A, B);
       else if (c.g.ndim == 3) k_big_rows<3><<<big_gx, 256, 0, g_bigs>>>(A, B);
       else k_big_rows<0><<<big_gx, 256, 0, g_bigs>>>(A, B);
-      k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B);
+      {
+        const char *e = getenv("LTS_LEVEL_MIN");
+        g_level_min = e ? atoi(e) : -1;
+      }
+      k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B, g_level_min);
       g_launches += 4;
-      LTS_TRY(big_iteration(c, A, B, big_gx));
+      // the level-parallel floods synchronise with the host: queue the main
+      // stream's work first (below) and run every iteration from the loop there
+      if (g_level_min < 0) LTS_TRY(big_iteration(c, A, B, big_gx));
+      else k_fill_int<<<1, 32, 0, g_bigs>>>(B.nactive, 1, 1);
     }
     A.qbase = nbig;
     if (R > nbig) {
