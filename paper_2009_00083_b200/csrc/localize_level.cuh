@@ -35,13 +35,17 @@
 // compared through j.  The neighbour keys of every key come from k_big_setup
 // (BigArgs::nrowkey), as for the CTA floods.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "localize_big.cuh"
 
 namespace lts {
 
+namespace cg = cooperative_groups;
+
 constexpr int LV_DONE = -1;
 constexpr unsigned LV_NONE = 0xffffffffu;
-enum { LVC_HOOKS = 0, LVC_CHANGED = 1, LVC_ACTIVE = 2, LVC_ERR = 3, LVC_N = 8 };
+enum { LVC_HOOKS = 0, LVC_CHANGED = 1, LVC_ACTIVE = 2, LVC_ERR = 3, LVC_N = 12 };
 
 struct LvArgs {
   int *task;    // j: source (j index) of the flood task the vertex belongs to, LV_DONE when placed
@@ -50,8 +54,9 @@ struct LvArgs {
   int *comp;    // j: component label (= j of the component's tree root) at round start
   int *link;    // labels: hook target of this round
   int *csize;   // j: class size (F-subtree size) of a trunk vertex
-  int *off;     // j: level-1 source mark during the flood
-  int *skey, *sval, *oval;  // final sort / scan buffers
+  int *lvl;     // j: level at which the vertex was placed (-2: not yet; sources: 0)
+  int *skey, *sval, *oval;  // final sort / scan buffers; during the levels skey = chain end of a source,
+                            // sval = task whose root component a placed chain vertex / ascending source joins
   unsigned long long *best;  // labels: best outgoing edge (min j, max j | INF)
   unsigned long long *pm;    // j: (value, ancestor) pairs of the two pointer-jumping phases
   int *ctr;
@@ -88,9 +93,25 @@ __device__ __forceinline__ unsigned long long lv_pack(unsigned hi, unsigned lo) 
   return ((unsigned long long)hi << 32) | lo;
 }
 
+// Every phase is a device function over the key space, strided by the caller:
+// a kernel of its own on the host-driven path, a stage between grid barriers
+// in the cooperative kernel.
+#define LV_FOR(j, L) for (int j = t0; j < (L).nj; j += nt)
+
+template <int K>
+__device__ __forceinline__ void lv_load_row(const BigArgs &Bg, const LvRef &R, int j, int (&q)[K]) {
+  const int2 *row = reinterpret_cast<const int2 *>(Bg.nrowkey + ((size_t)R.lo + R.rid + (j - R.jb)) * K);
+#pragma unroll
+  for (int h = 0; h < K / 2; h++) {
+    const int2 v = row[h];
+    q[2 * h] = v.x;
+    q[2 * h + 1] = v.y;
+  }
+}
+
 // sources of the coming ascending flood, per region (flat over big-region slots)
-__global__ void __launch_bounds__(256) k_lv_nsrc(LocArgs A, BigArgs Bg) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Bg.bslots; i += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_nsrc(const LocArgs &A, const BigArgs &Bg, int t0, int nt) {
+  for (int i = t0; i < Bg.bslots; i += nt) {
     const int qi = big_locate(Bg, i);
     int *st = Bg.st + qi * BST_W;
     if (!st[BST_ACTIVE] || !st[BST_LEVEL] || !(st[BST_T] & 1)) continue;
@@ -102,44 +123,88 @@ __global__ void __launch_bounds__(256) k_lv_nsrc(LocArgs A, BigArgs Bg) {
 
 // tasks of level 1: every vertex of a flooding region belongs to the task of
 // the region's source (desc) or virtual root (asc, at the unused key k)
-__global__ void __launch_bounds__(256) k_lv_init(LocArgs A, BigArgs Bg, LvArgs L) {
+__device__ __forceinline__ void lv_init(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, int *active_ctr, int t0,
+                                        int nt) {
   int mine = 0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
-    L.task[j] = LV_DONE;
-    L.fp[j] = LV_NONE;
-    L.off[j] = 0;
-    L.csize[j] = 0;
+  LV_FOR(j, L) {
+    int task = LV_DONE, lvl = -2, csz = 0, croot = -1;
     const LvRef R = lv_ref(A, Bg, j);
-    if (!R.active) continue;
-    const int kap = j - R.jb;
-    const int *cin = big_buf(A, R.t) + R.lo;
-    if (R.asc) {
-      if (Bg.st[R.qi * BST_W + BST_NSRC] == 0) continue;  // empty ascending flood: labels kept
-      if (kap == R.k) continue;                           // the virtual root
-      const int p = Bg.inv[R.lo + R.rid + kap];
-      L.task[j] = R.jb + R.k;
-      if (p >= 1 && (A.sfl[R.lo + p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) L.off[j] = 1;
-      mine++;
-    } else {
-      const int unused = R.t == 0 ? Bg.v0[R.qi] : R.k;
-      const int src = flood_key(cin[0], false, R.k);
-      if (kap == unused || kap == src) continue;
-      L.task[j] = R.jb + src;
-      mine++;
+    if (R.active) {
+      const int kap = j - R.jb;
+      const int *cin = big_buf(A, R.t) + R.lo;
+      if (R.asc) {
+        // an empty ascending flood keeps the labels; key k is the virtual root
+        if (Bg.st[R.qi * BST_W + BST_NSRC] != 0 && kap != R.k) {
+          const int p = Bg.inv[R.lo + R.rid + kap];
+          task = R.jb + R.k;
+          if (p >= 1 && (A.sfl[R.lo + p] & (SF_MIN | SF_OUT)) == (SF_MIN | SF_OUT)) croot = task;
+          mine++;
+        }
+      } else {
+        const int unused = R.t == 0 ? Bg.v0[R.qi] : R.k;
+        const int src = flood_key(cin[0], false, R.k);
+        if (kap == src) {
+          lvl = 0;
+          csz = R.k;  // a source with a class: its ascent chain is contracted at level 1
+        } else if (kap != unused) {
+          task = R.jb + src;
+          mine++;
+        }
+      }
     }
+    L.task[j] = task;
+    L.fp[j] = LV_NONE;
+    L.lvl[j] = lvl;
+    L.csize[j] = csz;
+    L.sval[j] = croot;
+    L.skey[j] = j;
   }
   mine = __reduce_add_sync(0xffffffffu, mine);
-  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(L.ctr + LVC_ACTIVE, mine);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(active_ctr, mine);
 }
 
-// per level: singleton components, no tree edges; the level-1 sources of an
-// ascending flood start inside the root's component
-__global__ void __launch_bounds__(256) k_lv_prep(LvArgs L) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+// Ascent contraction.  The flood of a task starts at its source p with the
+// highest member neighbour z1 of p, and continues z1 < z2 < ... as long as the
+// highest unplaced member neighbour of the last vertex is higher than it (it
+// then beats every older frontier key).  The chain is placed at once: F-parent
+// of z(i+1) is z(i), and the rest of the task floods from the sources
+// {p, z1, .., zm} together (they all count as +infinity).  One thread per task.
+template <int K>
+__device__ __forceinline__ void lv_chain(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, int t0, int nt) {
+  LV_FOR(p, L) {
+    if (L.lvl[p] != L.level - 1 || L.csize[p] <= 1 || L.task[p] != LV_DONE) continue;
+    const LvRef R = lv_ref(A, Bg, p);
+    int cur = p, last = -1;
+    for (;;) {
+      int q[K];
+      lv_load_row<K>(Bg, R, cur, q);
+      int z = -1;
+#pragma unroll
+      for (int kk = 0; kk < K; kk++) {
+        if (q[kk] < 0) continue;
+        const int u = R.jb + q[kk];
+        if (u > z && L.task[u] == p) z = u;
+      }
+      if (z < 0 || z < last) break;
+      L.task[z] = LV_DONE;
+      L.fp[z] = (unsigned)cur;
+      L.lvl[z] = L.level;
+      L.csize[z] = 1;
+      L.sval[z] = p;
+      last = cur = z;
+    }
+    L.skey[p] = cur;
+  }
+}
+
+// per level: singleton components, no tree edges; the sources of an ascending
+// flood start inside the (virtual) root's component
+__device__ __forceinline__ void lv_prep(const LvArgs &L, int t0, int nt) {
+  LV_FOR(j, L) {
     const int tk = L.task[j];
     if (tk < 0) continue;
     int c = j, p = -1;
-    if (L.level == 1 && L.off[j] == 1) c = p = tk;
+    if (L.sval[j] == tk) c = p = tk;
     L.comp[j] = c;
     L.link[j] = j;
     L.par[j] = p;
@@ -152,35 +217,31 @@ __global__ void __launch_bounds__(256) k_lv_prep(LvArgs L) {
 
 // Boruvka round, step 1: every vertex outside its task's root component offers
 // its heaviest edge leaving its component (weight: (min j, max j), the root
-// counting as +infinity) to the component's label
+// and its contracted chain counting as +infinity) to the component's label
 template <int K>
-__global__ void __launch_bounds__(256) k_lv_scan(LocArgs A, BigArgs Bg, LvArgs L) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_scan(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, int t0, int nt) {
+  LV_FOR(j, L) {
     const int tk = L.task[j];
     if (tk < 0) continue;
     const int c = L.comp[j];
     if (c == tk) continue;
     const LvRef R = lv_ref(A, Bg, j);
-    const int2 *row = reinterpret_cast<const int2 *>(Bg.nrowkey + ((size_t)R.lo + R.rid + (j - R.jb)) * K);
     int q[K];
-#pragma unroll
-    for (int h = 0; h < K / 2; h++) {
-      const int2 v = row[h];
-      q[2 * h] = v.x;
-      q[2 * h + 1] = v.y;
-    }
+    lv_load_row<K>(Bg, R, j, q);
     unsigned long long b = 0ull;
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
       if (q[kk] < 0) continue;
       const int u = R.jb + q[kk];
+      const int tu = L.task[u];
       unsigned long long w;
-      if (u == tk) {
-        w = lv_pack((unsigned)j, LV_NONE);
-      } else {
-        if (L.task[u] != tk) continue;
+      if (tu == tk) {
         if (L.comp[u] == c) continue;
         w = lv_pack((unsigned)min(u, j), (unsigned)max(u, j));
+      } else if (tu < 0 && (u == tk || L.sval[u] == tk)) {
+        w = lv_pack((unsigned)j, LV_NONE);
+      } else {
+        continue;
       }
       b = max(b, w);
     }
@@ -192,9 +253,9 @@ __global__ void __launch_bounds__(256) k_lv_scan(LocArgs A, BigArgs Bg, LvArgs L
 // tree path from the hook vertex to the old root is reversed, so the merged
 // tree stays rooted at the target's root.  Two components choosing the same
 // edge: the larger label hooks.
-__global__ void __launch_bounds__(256) k_lv_hook(LvArgs L) {
+__device__ __forceinline__ void lv_hook(const LvArgs &L, int *hook_ctr, int t0, int nt) {
   int hooks = 0;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.nj; c += gridDim.x * blockDim.x) {
+  LV_FOR(c, L) {
     const int tk = L.task[c];
     if (tk < 0 || L.comp[c] != c) continue;
     const unsigned long long e = L.best[c];
@@ -222,12 +283,12 @@ __global__ void __launch_bounds__(256) k_lv_hook(LvArgs L) {
     hooks++;
   }
   hooks = __reduce_add_sync(0xffffffffu, hooks);
-  if ((threadIdx.x & 31) == 0 && hooks) atomicAdd(L.ctr + LVC_HOOKS, hooks);
+  if ((threadIdx.x & 31) == 0 && hooks) atomicAdd(hook_ctr, hooks);
 }
 
 // step 3: labels of the merged components (the label is the tree root)
-__global__ void __launch_bounds__(256) k_lv_jump(LvArgs L) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_jump(const LvArgs &L, int t0, int nt) {
+  LV_FOR(j, L) {
     if (L.task[j] < 0) continue;
     const int c = L.comp[j];
     int r = c, nx;
@@ -244,16 +305,16 @@ __global__ void __launch_bounds__(256) k_lv_jump(LvArgs L) {
 }
 
 // beta: (smallest j on the tree path so far, ancestor reached)
-__global__ void __launch_bounds__(256) k_lv_pm_init(LvArgs L) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_pm_init(const LvArgs &L, int t0, int nt) {
+  LV_FOR(j, L) {
     if (L.task[j] < 0) continue;
     L.pm[j] = lv_pack((unsigned)j, (unsigned)L.par[j]);
   }
 }
 
-__global__ void __launch_bounds__(256) k_lv_pm_round(LvArgs L) {
+__device__ __forceinline__ void lv_pm_round(const LvArgs &L, int *changed, int t0, int nt) {
   int ch = 0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+  LV_FOR(j, L) {
     const int tk = L.task[j];
     if (tk < 0) continue;
     const unsigned long long a = L.pm[j];
@@ -264,21 +325,22 @@ __global__ void __launch_bounds__(256) k_lv_pm_round(LvArgs L) {
     L.pm[j] = lv_pack(m, (unsigned)(b & 0xffffffffu));
     ch = 1;
   }
-  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) L.ctr[LVC_CHANGED] = 1;
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
 
-// classes of this level: trunk vertices are placed (F-parent = task source),
-// the others join the task of their class's trunk vertex
-__global__ void __launch_bounds__(256) k_lv_classes(LvArgs L) {
+// classes of this level: trunk vertices are placed (F-parent = the end of the
+// task source's chain), the others join the task of their class's trunk vertex
+__device__ __forceinline__ void lv_classes(const LvArgs &L, int *active_ctr, int t0, int nt) {
   int act = 0;
-  for (int j0 = blockIdx.x * blockDim.x; j0 < L.nj; j0 += gridDim.x * blockDim.x) {
-    const int j = j0 + threadIdx.x;
+  for (int j0 = t0 - (int)(threadIdx.x & 31); j0 < L.nj; j0 += nt) {
+    const int j = j0 + (threadIdx.x & 31);
     const int tk = j < L.nj ? L.task[j] : -1;
     int beta = -1;
     if (tk >= 0) {
       beta = (int)(L.pm[j] >> 32);
       if (beta == j) {
-        L.fp[j] = (unsigned)tk;
+        L.fp[j] = (unsigned)L.skey[tk];
+        L.lvl[j] = L.level;
         L.task[j] = LV_DONE;
       } else {
         L.task[j] = beta;
@@ -290,12 +352,12 @@ __global__ void __launch_bounds__(256) k_lv_classes(LvArgs L) {
     if (beta >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(L.csize + beta, __popc(peers));
   }
   act = __reduce_add_sync(0xffffffffu, act);
-  if ((threadIdx.x & 31) == 0 && act) atomicAdd(L.ctr + LVC_ACTIVE, act);
+  if ((threadIdx.x & 31) == 0 && act) atomicAdd(active_ctr, act);
 }
 
 // ---- extraction indices: preorder of F, children in decreasing key ----------
-__global__ void __launch_bounds__(256) k_lv_sortkeys(LvArgs L) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.nj; i += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_sortkeys(const LvArgs &L, int t0, int nt) {
+  LV_FOR(i, L) {
     const int j = L.nj - 1 - i;
     const unsigned f = L.fp[j];
     L.skey[i] = f == LV_NONE ? L.nj : (int)f;
@@ -303,8 +365,8 @@ __global__ void __launch_bounds__(256) k_lv_sortkeys(LvArgs L) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_lv_gather(LvArgs L) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.nj; i += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_gather(const LvArgs &L, int t0, int nt) {
+  LV_FOR(i, L) {
     const int j = L.oval[i];
     L.skey[i] = L.fp[j] == LV_NONE ? 0 : L.csize[j];
   }
@@ -312,16 +374,16 @@ __global__ void __launch_bounds__(256) k_lv_gather(LvArgs L) {
 
 // cum = exclusive prefix of the class sizes in sorted order (in sval); the
 // first child of every parent records the parent's base
-__global__ void __launch_bounds__(256) k_lv_heads(LvArgs L) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.nj; i += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_heads(const LvArgs &L, int t0, int nt) {
+  LV_FOR(i, L) {
     const unsigned f = L.fp[L.oval[i]];
     if (f == LV_NONE) continue;
     if (i == 0 || L.fp[L.oval[i - 1]] != f) L.par[f] = L.sval[i];
   }
 }
 
-__global__ void __launch_bounds__(256) k_lv_off(LocArgs A, BigArgs Bg, LvArgs L) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.nj; i += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_off(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, int t0, int nt) {
+  LV_FOR(i, L) {
     const int j = L.oval[i];
     const unsigned f = L.fp[j];
     if (f == LV_NONE) continue;
@@ -331,9 +393,9 @@ __global__ void __launch_bounds__(256) k_lv_off(LocArgs A, BigArgs Bg, LvArgs L)
   }
 }
 
-__global__ void __launch_bounds__(256) k_lv_pos_round(LvArgs L) {
+__device__ __forceinline__ void lv_pos_round(const LvArgs &L, int *changed, int t0, int nt) {
   int ch = 0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+  LV_FOR(j, L) {
     if (L.fp[j] == LV_NONE) continue;
     const unsigned long long a = L.pm[j];
     const unsigned anc = (unsigned)(a & 0xffffffffu);
@@ -342,12 +404,12 @@ __global__ void __launch_bounds__(256) k_lv_pos_round(LvArgs L) {
     L.pm[j] = lv_pack((unsigned)(a >> 32) + (unsigned)(b >> 32), (unsigned)(b & 0xffffffffu));
     ch = 1;
   }
-  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) L.ctr[LVC_CHANGED] = 1;
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
 
 // state t+1 of every level-flooded region
-__global__ void __launch_bounds__(256) k_lv_write(LocArgs A, BigArgs Bg, LvArgs L) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L.nj; j += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void lv_write(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, int t0, int nt) {
+  LV_FOR(j, L) {
     const LvRef R = lv_ref(A, Bg, j);
     if (!R.active) continue;
     const int kap = j - R.jb;
@@ -363,6 +425,89 @@ __global__ void __launch_bounds__(256) k_lv_write(LocArgs A, BigArgs Bg, LvArgs 
     const int e = L.fp[j] == LV_NONE ? 0 : (int)(L.pm[j] >> 32);
     cout[p] = R.asc ? e : R.k - 1 - e;
     if (p == 0) atomicAdd(Bg.work, (unsigned long long)R.k);
+  }
+}
+
+#define LV_T0 (int)(blockIdx.x * blockDim.x + threadIdx.x)
+#define LV_NT (int)(gridDim.x * blockDim.x)
+__global__ void __launch_bounds__(256) k_lv_nsrc(LocArgs A, BigArgs Bg) { lv_nsrc(A, Bg, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_init(LocArgs A, BigArgs Bg, LvArgs L) {
+  lv_init(A, Bg, L, L.ctr + LVC_ACTIVE, LV_T0, LV_NT);
+}
+template <int K>
+__global__ void __launch_bounds__(256) k_lv_chain(LocArgs A, BigArgs Bg, LvArgs L) { lv_chain<K>(A, Bg, L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_prep(LvArgs L) { lv_prep(L, LV_T0, LV_NT); }
+template <int K>
+__global__ void __launch_bounds__(256) k_lv_scan(LocArgs A, BigArgs Bg, LvArgs L) { lv_scan<K>(A, Bg, L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_hook(LvArgs L) { lv_hook(L, L.ctr + LVC_HOOKS, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_jump(LvArgs L) { lv_jump(L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_pm_init(LvArgs L) { lv_pm_init(L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_pm_round(LvArgs L) { lv_pm_round(L, L.ctr + LVC_CHANGED, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_classes(LvArgs L) { lv_classes(L, L.ctr + LVC_ACTIVE, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_sortkeys(LvArgs L) { lv_sortkeys(L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_gather(LvArgs L) { lv_gather(L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_heads(LvArgs L) { lv_heads(L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_off(LocArgs A, BigArgs Bg, LvArgs L) { lv_off(A, Bg, L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_pos_round(LvArgs L) { lv_pos_round(L, L.ctr + LVC_CHANGED, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_write(LocArgs A, BigArgs Bg, LvArgs L) { lv_write(A, Bg, L, LV_T0, LV_NT); }
+
+// All levels of one flood in one cooperative launch: the phases are separated
+// by grid barriers and the loop conditions are read on the device.  A counter
+// slot is cleared only after every thread has read it and passed a barrier:
+// the hook counter alternates between two slots (read before the round's last
+// barrier), the changed flag rotates over three (read after its barrier), the
+// active count alternates by level.
+enum { LVK_HOOKS = 0, LVK_CHANGED = 2, LVK_ACTIVE = 5, LVK_INIT = 7, LVK_LEVELS = 8, LVK_ROUNDS = 9 };
+
+template <int K>
+__global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L) {
+  cg::grid_group grid = cg::this_grid();
+  const int t0 = LV_T0, nt = LV_NT;
+  const bool lead = t0 == 0;
+  int *ctr = L.ctr;  // zeroed by the host
+  lv_nsrc(A, Bg, t0, nt);
+  grid.sync();
+  lv_init(A, Bg, L, ctr + LVK_INIT, t0, nt);
+  grid.sync();
+  int active = *(volatile int *)(ctr + LVK_INIT);
+  int rounds = 0, cslot = 0;
+  L.level = 0;
+  while (active > 0) {
+    L.level++;
+    const int apar = L.level & 1;
+    lv_chain<K>(A, Bg, L, t0, nt);
+    grid.sync();
+    lv_prep(L, t0, nt);
+    if (lead) ctr[LVK_ACTIVE + apar] = 0;
+    grid.sync();
+    for (int round = 0; round < 64; round++, rounds++) {
+      const int hp = round & 1;
+      lv_scan<K>(A, Bg, L, t0, nt);
+      if (lead) ctr[LVK_HOOKS + (hp ^ 1)] = 0;
+      grid.sync();
+      lv_hook(L, ctr + LVK_HOOKS + hp, t0, nt);
+      grid.sync();
+      lv_jump(L, t0, nt);
+      const int h = *(volatile int *)(ctr + LVK_HOOKS + hp);
+      grid.sync();
+      if (h == 0) break;
+    }
+    lv_pm_init(L, t0, nt);
+    grid.sync();
+    for (int it = 0; it < 64; it++) {
+      cslot = cslot == 2 ? 0 : cslot + 1;
+      if (lead) ctr[LVK_CHANGED + (cslot == 2 ? 0 : cslot + 1)] = 0;
+      lv_pm_round(L, ctr + LVK_CHANGED + cslot, t0, nt);
+      grid.sync();
+      if (*(volatile int *)(ctr + LVK_CHANGED + cslot) == 0) break;
+    }
+    lv_classes(L, ctr + LVK_ACTIVE + apar, t0, nt);
+    grid.sync();
+    active = *(volatile int *)(ctr + LVK_ACTIVE + apar);
+  }
+  if (lead) {
+    ctr[LVK_LEVELS] = L.level;
+    ctr[LVK_ROUNDS] = rounds;
   }
 }
 

@@ -153,6 +153,7 @@ struct DevState {
   cudaEvent_t fork = nullptr, join = nullptr;
   bool big_attr = false;
   int coop_blocks = 0;
+  int lv_blocks[4] = {0, 0, 0, 0};  // cooperative grid of the level-parallel floods, per ndim
 };
 static DevState g_dev[LTS_MAX_DEV];
 static DevState *g_cur = &g_dev[0];
@@ -255,8 +256,8 @@ enum {
   SC_BIGWORK = 34,  // 2 ints: 64-bit sum of region sizes flooded by k_big_flood
   SC_BIGSLOTS = 36, // = SC_NBIG + 7: slots of the big regions
   SC_BVSTATE = 40,  // 2: active roots of the last Boruvka round, rounds run
-  SC_LV = 44,       // LVC_N counters of the level-parallel floods
-  SC_LVTMP = 52,
+  SC_LV = 44,       // LVC_N (12) counters of the level-parallel floods
+  SC_LVTMP = 56,
   SC_N = 64
 };
 
@@ -311,7 +312,7 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
     // key space of the large regions: one entry per slot plus one per region
     const int64_t nj = s2 + n1 / BIG_THRESHOLD + 8;
     w->lv.task = i32(nj); w->lv.fp = u32(nj); w->lv.par = i32(nj); w->lv.comp = i32(nj); w->lv.link = i32(nj);
-    w->lv.csize = i32(nj); w->lv.off = i32(nj); w->lv.skey = i32(nj); w->lv.sval = i32(nj); w->lv.oval = i32(nj);
+    w->lv.csize = i32(nj); w->lv.lvl = i32(nj); w->lv.skey = i32(nj); w->lv.sval = i32(nj); w->lv.oval = i32(nj);
     w->lv.best = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)nj);
     w->lv.pm = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)nj);
     // the final sort runs after the levels: its ping-pong buffers reuse the Boruvka arrays
@@ -605,47 +606,70 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
   const int gj = (int)std::min<int64_t>(((int64_t)L.nj + 255) / 256, 148 * 8);
   const int gs = (int)std::min<int64_t>(((int64_t)B.bslots + 255) / 256, 148 * 8);
   int *hc = c.h_scal + SC_LV;
-  LTS_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(int) * LVC_N, s));
-  k_lv_nsrc<<<gs, 256, 0, s>>>(A, B);
-  k_lv_init<<<gj, 256, 0, s>>>(A, B, L);
-  g_launches += 2;
-  LTS_TRY(lv_read(c, LVC_ACTIVE, 1));
-  int active = hc[LVC_ACTIVE];
   int levels = 0, rounds_total = 0;
-  while (active > 0) {
-    L.level = ++levels;
-    k_lv_prep<<<gj, 256, 0, s>>>(L);
-    g_launches++;
-    for (int round = 0;; round++) {
-      if (round >= 64) return lts_set_error(LTS_E_CUDA, "level flood: spanning forest did not converge");
-      LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_HOOKS, 0, sizeof(int), s));
-      if (c.g.ndim == 2) k_lv_scan<6><<<gj, 256, 0, s>>>(A, B, L);
-      else if (c.g.ndim == 3) k_lv_scan<14><<<gj, 256, 0, s>>>(A, B, L);
-      else k_lv_scan<kCsrK><<<gj, 256, 0, s>>>(A, B, L);
-      k_lv_hook<<<gj, 256, 0, s>>>(L);
-      k_lv_jump<<<gj, 256, 0, s>>>(L);
-      g_launches += 3;
-      rounds_total++;
-      LTS_TRY(lv_read(c, LVC_HOOKS, 1));
-      if (hc[LVC_HOOKS] == 0) break;
+  LTS_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(int) * LVC_N, s));
+  static const bool host_loop = getenv("LTS_LEVEL_HOST") != nullptr;
+  const int nd = c.g.ndim;
+  if (!host_loop) {
+    // every level in one cooperative launch
+    DevState &d = *g_cur;
+    const void *fn = nd == 2 ? (const void *)k_lv_coop<6> : nd == 3 ? (const void *)k_lv_coop<14>
+                                                                   : (const void *)k_lv_coop<kCsrK>;
+    if (!d.lv_blocks[nd]) {
+      int dev = 0, nsm = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      LTS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 512, 0));
+      d.lv_blocks[nd] = std::max(1, std::min(per, 1)) * nsm;
     }
-    k_lv_pm_init<<<gj, 256, 0, s>>>(L);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(d.lv_blocks[nd], ((int64_t)L.nj + 511) / 512));
+    void *kargs[] = {(void *)&A, (void *)&B, (void *)&L};
+    LTS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), kargs, 0, s));
     g_launches++;
-    for (int it = 0;; it++) {
-      if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: path minima did not converge");
-      LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
-      k_lv_pm_round<<<gj, 256, 0, s>>>(L);
-      k_lv_pm_round<<<gj, 256, 0, s>>>(L);
-      g_launches += 2;
-      LTS_TRY(lv_read(c, LVC_CHANGED, 1));
-      if (hc[LVC_CHANGED] == 0) break;
-    }
-    LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_ACTIVE, 0, sizeof(int), s));
-    k_lv_classes<<<gj, 256, 0, s>>>(L);
-    g_launches++;
+  } else {
+    k_lv_nsrc<<<gs, 256, 0, s>>>(A, B);
+    k_lv_init<<<gj, 256, 0, s>>>(A, B, L);
+    g_launches += 2;
     LTS_TRY(lv_read(c, LVC_ACTIVE, 1));
-    if (hc[LVC_ACTIVE] >= active) return lts_set_error(LTS_E_CUDA, "level flood: no progress");
-    active = hc[LVC_ACTIVE];
+    int active = hc[LVC_ACTIVE];
+    while (active > 0) {
+      L.level = ++levels;
+      if (nd == 2) k_lv_chain<6><<<gj, 256, 0, s>>>(A, B, L);
+      else if (nd == 3) k_lv_chain<14><<<gj, 256, 0, s>>>(A, B, L);
+      else k_lv_chain<kCsrK><<<gj, 256, 0, s>>>(A, B, L);
+      k_lv_prep<<<gj, 256, 0, s>>>(L);
+      g_launches += 2;
+      for (int round = 0;; round++) {
+        if (round >= 64) return lts_set_error(LTS_E_CUDA, "level flood: spanning forest did not converge");
+        LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_HOOKS, 0, sizeof(int), s));
+        if (nd == 2) k_lv_scan<6><<<gj, 256, 0, s>>>(A, B, L);
+        else if (nd == 3) k_lv_scan<14><<<gj, 256, 0, s>>>(A, B, L);
+        else k_lv_scan<kCsrK><<<gj, 256, 0, s>>>(A, B, L);
+        k_lv_hook<<<gj, 256, 0, s>>>(L);
+        k_lv_jump<<<gj, 256, 0, s>>>(L);
+        g_launches += 3;
+        rounds_total++;
+        LTS_TRY(lv_read(c, LVC_HOOKS, 1));
+        if (hc[LVC_HOOKS] == 0) break;
+      }
+      k_lv_pm_init<<<gj, 256, 0, s>>>(L);
+      g_launches++;
+      for (int it = 0;; it++) {
+        if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: path minima did not converge");
+        LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
+        k_lv_pm_round<<<gj, 256, 0, s>>>(L);
+        k_lv_pm_round<<<gj, 256, 0, s>>>(L);
+        g_launches += 2;
+        LTS_TRY(lv_read(c, LVC_CHANGED, 1));
+        if (hc[LVC_CHANGED] == 0) break;
+      }
+      LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_ACTIVE, 0, sizeof(int), s));
+      k_lv_classes<<<gj, 256, 0, s>>>(L);
+      g_launches++;
+      LTS_TRY(lv_read(c, LVC_ACTIVE, 1));
+      if (hc[LVC_ACTIVE] >= active) return lts_set_error(LTS_E_CUDA, "level flood: no progress");
+      active = hc[LVC_ACTIVE];
+    }
   }
   // extraction index = preorder of F, children in decreasing key
   k_lv_sortkeys<<<gj, 256, 0, s>>>(L);
@@ -668,7 +692,14 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
   k_lv_write<<<gj, 256, 0, s>>>(A, B, L);
   g_launches++;
   static const bool verbose = getenv("LTS_LEVEL_VERBOSE") != nullptr;
-  if (verbose) fprintf(stderr, "[lts] level flood: nj %d levels %d boruvka rounds %d\n", L.nj, levels, rounds_total);
+  if (verbose) {
+    if (!host_loop) {
+      LTS_TRY(lv_read(c, LVK_LEVELS, 2));
+      levels = hc[LVK_LEVELS];
+      rounds_total = hc[LVK_ROUNDS];
+    }
+    fprintf(stderr, "[lts] level flood: nj %d levels %d boruvka rounds %d\n", L.nj, levels, rounds_total);
+  }
   LTS_KCHECK();
   return 0;
 }
