@@ -76,7 +76,8 @@ __device__ __forceinline__ int big_locate(const BigArgs &Bg, int i) {
 // setup / check kernels and the one-CTA-per-region flood kernel
 // BST_NSRC: sources of the coming ascending flood; BST_LEVEL: the region floods
 // level-parallel (localize_level.cuh) instead of in k_big_flood
-enum { BST_T = 0, BST_ACTIVE, BST_FIN, BST_STATUS, BST_BAD, BST_DIFF, BST_NSRC, BST_LEVEL, BST_W = 8 };
+// BST_NMAX: local maxima of the region's initial order (its roughness)
+enum { BST_T = 0, BST_ACTIVE, BST_FIN, BST_STATUS, BST_BAD, BST_DIFF, BST_NSRC, BST_LEVEL, BST_NMAX, BST_W = 12 };
 
 // optional per-region instrumentation (lts_debug_big_stats): big-queue slot i
 // records [k, frontier steps, candidates, committed, flood cycles, global-rule
@@ -723,6 +724,7 @@ __global__ void __launch_bounds__(256) k_big_rows(LocArgs A, BigArgs Bg) {
     const int i = b0 + threadIdx.x;
     const int qi = i < Bg.bslots ? big_locate(Bg, i) : -1;
     int mine = 0x7fffffff;
+    bool ismax = false;
     if (qi >= 0) {
       const int rid = A.order[Bg.qbase + qi];
       const int lo = A.rptr[rid];
@@ -730,21 +732,28 @@ __global__ void __launch_bounds__(256) k_big_rows(LocArgs A, BigArgs Bg) {
       const int s = A.verts[lo];
       const int srank = eff_rank(A.rank, s, A.rev, n);
       const Nb<NDIM> nb(A.g, A.verts[lo + p]);
-      bool out = false;
+      bool out = false, top = p >= 1;
       int *row = Bg.nrow + ((size_t)lo + p) * K;
 #pragma unroll
       for (int kk = 0; kk < K; kk++) {
         int u = nb(A.g, kk);
-        row[kk] = member(A, u, rid, s);
+        const int q = member(A, u, rid, s);
+        row[kk] = q;
+        if (q > p) top = false;
         if (p >= 1 && u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) out = true;
       }
       A.sfl[lo + p] = out ? SF_OUT : 0;
       if (out) mine = p;
+      ismax = top;
       A.buf0[lo + p] = p;
     }
     const unsigned peers = __match_any_sync(0xffffffffu, qi);
     const int m = __reduce_min_sync(peers, mine);
-    if (qi >= 0 && lane == __ffs(peers) - 1 && m != 0x7fffffff) atomicMin(Bg.v0 + qi, m);
+    const int nm = __popc(__ballot_sync(0xffffffffu, ismax) & peers);
+    if (qi >= 0 && lane == __ffs(peers) - 1) {
+      if (m != 0x7fffffff) atomicMin(Bg.v0 + qi, m);
+      if (nm) atomicAdd(Bg.st + qi * BST_W + BST_NMAX, nm);
+    }
   }
 }
 
@@ -809,7 +818,7 @@ __device__ __forceinline__ BigRef big_ref(const LocArgs &A, const BigArgs &Bg, i
 }
 
 // per region: v0 from k_big_rows; no admissible minimum -> status 1
-__global__ void k_big_init(LocArgs A, BigArgs Bg, int level_min) {
+__global__ void k_big_init(LocArgs A, BigArgs Bg, int level_min, int level_ratio, int *nlevel) {
   GRID_STRIDE(qi, Bg.nbig) {
     const BigRef R = big_ref(A, Bg, (int)qi);
     const int v0 = Bg.v0[qi];
@@ -818,7 +827,10 @@ __global__ void k_big_init(LocArgs A, BigArgs Bg, int level_min) {
     st[BST_BAD] = 0;
     st[BST_DIFF] = 0;
     st[BST_NSRC] = 0;
-    st[BST_LEVEL] = level_min >= 0 && R.k >= level_min ? 1 : 0;
+    // rough regions (many local maxima per vertex) flood level-parallel
+    const int lev = level_min >= 0 && R.k >= level_min && (long long)st[BST_NMAX] * level_ratio >= R.k ? 1 : 0;
+    st[BST_LEVEL] = lev;
+    if (lev) atomicAdd(nlevel, 1);
     if (v0 == 0x7fffffff) {
       st[BST_ACTIVE] = 0;
       st[BST_FIN] = -1;

@@ -459,11 +459,21 @@ __global__ void __launch_bounds__(256) k_lv_write(LocArgs A, BigArgs Bg, LvArgs 
 // active count alternates by level.
 enum { LVK_HOOKS = 0, LVK_CHANGED = 2, LVK_ACTIVE = 5, LVK_INIT = 7, LVK_LEVELS = 8, LVK_ROUNDS = 9 };
 
+// phase clocks of the lead thread (LTS_LEVEL_VERBOSE): chain, prep, scan, hook, jump, beta, classes
+__device__ long long d_lvclk[8];
+#define LV_TICK(i)                 \
+  if (lead) {                      \
+    const long long tn = clock64(); \
+    d_lvclk[i] += tn - tq;         \
+    tq = tn;                       \
+  }
+
 template <int K>
 __global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L) {
   cg::grid_group grid = cg::this_grid();
   const int t0 = LV_T0, nt = LV_NT;
   const bool lead = t0 == 0;
+  long long tq = clock64();
   int *ctr = L.ctr;  // zeroed by the host
   lv_nsrc(A, Bg, t0, nt);
   grid.sync();
@@ -475,21 +485,27 @@ __global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L
   while (active > 0) {
     L.level++;
     const int apar = L.level & 1;
+    LV_TICK(7)
     lv_chain<K>(A, Bg, L, t0, nt);
     grid.sync();
+    LV_TICK(0)
     lv_prep(L, t0, nt);
     if (lead) ctr[LVK_ACTIVE + apar] = 0;
     grid.sync();
+    LV_TICK(1)
     for (int round = 0; round < 64; round++, rounds++) {
       const int hp = round & 1;
       lv_scan<K>(A, Bg, L, t0, nt);
       if (lead) ctr[LVK_HOOKS + (hp ^ 1)] = 0;
       grid.sync();
+      LV_TICK(2)
       lv_hook(L, ctr + LVK_HOOKS + hp, t0, nt);
       grid.sync();
+      LV_TICK(3)
       lv_jump(L, t0, nt);
       const int h = *(volatile int *)(ctr + LVK_HOOKS + hp);
       grid.sync();
+      LV_TICK(4)
       if (h == 0) break;
     }
     lv_pm_init(L, t0, nt);
@@ -501,13 +517,30 @@ __global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L
       grid.sync();
       if (*(volatile int *)(ctr + LVK_CHANGED + cslot) == 0) break;
     }
+    LV_TICK(5)
     lv_classes(L, ctr + LVK_ACTIVE + apar, t0, nt);
     grid.sync();
+    LV_TICK(6)
     active = *(volatile int *)(ctr + LVK_ACTIVE + apar);
   }
   if (lead) {
     ctr[LVK_LEVELS] = L.level;
     ctr[LVK_ROUNDS] = rounds;
+  }
+}
+
+// positions by pointer jumping over F, all rounds in one cooperative launch
+// (ctr[LVK_CHANGED..+2] zeroed by the host)
+__global__ void __launch_bounds__(512) k_lv_pos_coop(LvArgs L) {
+  cg::grid_group grid = cg::this_grid();
+  const int t0 = LV_T0, nt = LV_NT;
+  int cslot = 0;
+  for (int it = 0; it < 64; it++) {
+    cslot = cslot == 2 ? 0 : cslot + 1;
+    if (t0 == 0) L.ctr[LVK_CHANGED + (cslot == 2 ? 0 : cslot + 1)] = 0;
+    lv_pos_round(L, L.ctr + LVK_CHANGED + cslot, t0, nt);
+    grid.sync();
+    if (*(volatile int *)(L.ctr + LVK_CHANGED + cslot) == 0) break;
   }
 }
 

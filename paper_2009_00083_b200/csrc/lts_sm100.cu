@@ -149,11 +149,11 @@ struct DevState {
   int *h_scal = nullptr;  // pinned scalar readback slots
   std::vector<cudaEvent_t> events;
   size_t ev_next = 0;
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t side = nullptr, side2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, lfork = nullptr, ljoin = nullptr;
   bool big_attr = false;
   int coop_blocks = 0;
-  int lv_blocks[4] = {0, 0, 0, 0};  // cooperative grid of the level-parallel floods, per ndim
+  int lv_blocks[4] = {0, 0, 0, 0}, lv_per[4] = {0, 0, 0, 0};  // cooperative grid of the level floods, per ndim
 };
 static DevState g_dev[LTS_MAX_DEV];
 static DevState *g_cur = &g_dev[0];
@@ -512,6 +512,7 @@ __global__ void k_count_big(const int *rsize, int R, int th, int *out) {
 }
 
 static cudaStream_t g_bigs = nullptr;  // stream of the current call's large-region floods
+static cudaStream_t g_lvs = nullptr;   // stream of their level-parallel part (beside the CTA floods)
 
 static int big_stream_fork(cudaStream_t s) {
   DevState &d = *g_cur;
@@ -519,6 +520,9 @@ static int big_stream_fork(cudaStream_t s) {
     LTS_CUDA(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
     LTS_CUDA(cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming));
     LTS_CUDA(cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming));
+    LTS_CUDA(cudaStreamCreateWithFlags(&d.side2, cudaStreamNonBlocking));
+    LTS_CUDA(cudaEventCreateWithFlags(&d.lfork, cudaEventDisableTiming));
+    LTS_CUDA(cudaEventCreateWithFlags(&d.ljoin, cudaEventDisableTiming));
   }
   if (!d.big_attr) {
     LTS_CUDA(cudaFuncSetAttribute(k_big_flood<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
@@ -536,6 +540,7 @@ static int big_stream_fork(cudaStream_t s) {
   // stream, alone on the GPU
   static const bool serial = getenv("LTS_BIG_SERIAL") != nullptr;
   g_bigs = serial ? s : d.side;
+  g_lvs = serial ? s : d.side2;
   if (serial) return 0;
   LTS_CUDA(cudaEventRecord(d.fork, s));
   LTS_CUDA(cudaStreamWaitEvent(g_bigs, d.fork, 0));
@@ -552,7 +557,13 @@ static int big_stream_join(cudaStream_t s) {
 // one flood of every large region still flooding: grid-wide relabelling,
 // one CTA per region for the flood, grid-wide checks, per-region decision
 static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B);
-static int g_level_min = -1;  // regions of at least this many slots flood level-parallel (-1: none)
+// Flood policy: a large region floods level-parallel (localize_level.cuh) when it
+// is rough, i.e. has at least k / ratio local maxima in its initial order; smooth
+// regions keep the batched CTA flood (their level count grows with the length
+// of the climb).  LTS_LEVEL_MIN=-1 disables the level path, LTS_LEVEL_RATIO
+// moves the threshold.
+static int g_level_min = 0, g_level_ratio = 32;
+static int g_nlevel = 0;  // level-flooded regions of the current pass
 
 static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
   const int rg = gx;
@@ -566,10 +577,23 @@ static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
     fa = next_event();
     LTS_CUDA(cudaEventRecord(fa, g_bigs));
   }
-  if (c.g.ndim == 2) k_big_flood<2><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
-  else if (c.g.ndim == 3) k_big_flood<3><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
-  else k_big_flood<0><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
-  if (g_level_min >= 0) LTS_TRY(big_level_flood(c, A, B));
+  const bool lev = g_nlevel > 0;
+  if (lev && g_lvs != g_bigs) {  // the level-parallel floods run beside the CTA floods
+    LTS_CUDA(cudaEventRecord(g_cur->lfork, g_bigs));
+    LTS_CUDA(cudaStreamWaitEvent(g_lvs, g_cur->lfork, 0));
+  }
+  if (g_nlevel < B.nbig) {
+    if (c.g.ndim == 2) k_big_flood<2><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+    else if (c.g.ndim == 3) k_big_flood<3><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+    else k_big_flood<0><<<B.nbig, BIG_T, sizeof(BigSmem), g_bigs>>>(A, B);
+  }
+  if (lev) {
+    LTS_TRY(big_level_flood(c, A, B));
+    if (g_lvs != g_bigs) {
+      LTS_CUDA(cudaEventRecord(g_cur->ljoin, g_lvs));
+      LTS_CUDA(cudaStreamWaitEvent(g_bigs, g_cur->ljoin, 0));
+    }
+  }
   if (c.timing) {
     fb = next_event();
     LTS_CUDA(cudaEventRecord(fb, g_bigs));
@@ -591,8 +615,8 @@ static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
 // back on the flood stream.
 static int lv_read(Ctx &c, int first, int count) {
   LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_LV + first, c.w.scal + SC_LV + first, sizeof(int) * count,
-                           cudaMemcpyDeviceToHost, g_bigs));
-  LTS_CUDA(cudaStreamSynchronize(g_bigs));
+                           cudaMemcpyDeviceToHost, g_lvs));
+  LTS_CUDA(cudaStreamSynchronize(g_lvs));
   return 0;
 }
 
@@ -602,11 +626,11 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
   L.ctr = w.scal + SC_LV;
   L.nj = B.bslots + B.nbig;
   L.level = 0;
-  cudaStream_t s = g_bigs;
+  cudaStream_t s = g_lvs;
   const int gj = (int)std::min<int64_t>(((int64_t)L.nj + 255) / 256, 148 * 8);
   const int gs = (int)std::min<int64_t>(((int64_t)B.bslots + 255) / 256, 148 * 8);
   int *hc = c.h_scal + SC_LV;
-  int levels = 0, rounds_total = 0;
+  int levels = 0, rounds_total = 0, lv_grid = 1;
   LTS_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(int) * LVC_N, s));
   static const bool host_loop = getenv("LTS_LEVEL_HOST") != nullptr;
   const int nd = c.g.ndim;
@@ -620,11 +644,15 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       LTS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 512, 0));
-      d.lv_blocks[nd] = std::max(1, std::min(per, 1)) * nsm;
+      d.lv_blocks[nd] = nsm;
+      d.lv_per[nd] = std::max(1, per);
     }
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(d.lv_blocks[nd], ((int64_t)L.nj + 511) / 512));
+    // one block per SM keeps the grid barriers short; large key spaces take
+    // more blocks for memory parallelism
+    lv_grid = d.lv_blocks[nd] * std::min(d.lv_per[nd], L.nj >= (1 << 20) ? 2 : 1);
+    lv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(lv_grid, ((int64_t)L.nj + 511) / 512));
     void *kargs[] = {(void *)&A, (void *)&B, (void *)&L};
-    LTS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), kargs, 0, s));
+    LTS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(lv_grid), dim3(512), kargs, 0, s));
     g_launches++;
   } else {
     k_lv_nsrc<<<gs, 256, 0, s>>>(A, B);
@@ -680,14 +708,21 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
   k_lv_heads<<<gj, 256, 0, s>>>(L);
   k_lv_off<<<gj, 256, 0, s>>>(A, B, L);
   g_launches += 4;
-  for (int it = 0;; it++) {
-    if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: positions did not converge");
-    LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
-    k_lv_pos_round<<<gj, 256, 0, s>>>(L);
-    k_lv_pos_round<<<gj, 256, 0, s>>>(L);
-    g_launches += 2;
-    LTS_TRY(lv_read(c, LVC_CHANGED, 1));
-    if (hc[LVC_CHANGED] == 0) break;
+  if (!host_loop) {
+    LTS_CUDA(cudaMemsetAsync(L.ctr + LVK_CHANGED, 0, sizeof(int) * 3, s));
+    void *kargs[] = {(void *)&L};
+    LTS_CUDA(cudaLaunchCooperativeKernel((const void *)k_lv_pos_coop, dim3(lv_grid), dim3(512), kargs, 0, s));
+    g_launches++;
+  } else {
+    for (int it = 0;; it++) {
+      if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: positions did not converge");
+      LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
+      k_lv_pos_round<<<gj, 256, 0, s>>>(L);
+      k_lv_pos_round<<<gj, 256, 0, s>>>(L);
+      g_launches += 2;
+      LTS_TRY(lv_read(c, LVC_CHANGED, 1));
+      if (hc[LVC_CHANGED] == 0) break;
+    }
   }
   k_lv_write<<<gj, 256, 0, s>>>(A, B, L);
   g_launches++;
@@ -698,7 +733,13 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
       levels = hc[LVK_LEVELS];
       rounds_total = hc[LVK_ROUNDS];
     }
-    fprintf(stderr, "[lts] level flood: nj %d levels %d boruvka rounds %d\n", L.nj, levels, rounds_total);
+    long long clk[8];
+    cudaMemcpyFromSymbol(clk, d_lvclk, sizeof(clk));
+    fprintf(stderr, "[lts] level flood: nj %d levels %d boruvka rounds %d | Mcyc chain %.2f prep %.2f scan %.2f hook %.2f "
+            "jump %.2f beta %.2f classes %.2f\n", L.nj, levels, rounds_total, clk[0] / 1e6, clk[1] / 1e6, clk[2] / 1e6,
+            clk[3] / 1e6, clk[4] / 1e6, clk[5] / 1e6, clk[6] / 1e6);
+    memset(clk, 0, sizeof(clk));
+    cudaMemcpyToSymbol(d_lvclk, clk, sizeof(clk));
   }
   LTS_KCHECK();
   return 0;
@@ -884,6 +925,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       B.nactive = w.scal + SC_BIGACT;
       B.work = reinterpret_cast<unsigned long long *>(w.scal + SC_BIGWORK);
       k_fill_int<<<NB(nbig), 256, 0, g_bigs>>>(w.bigv0, nbig, 0x7fffffff);
+      LTS_CUDA(cudaMemsetAsync(w.bst, 0, sizeof(int) * BST_W * (size_t)nbig, g_bigs));
       k_big_prefix<<<1, 1024, 0, g_bigs>>>(A, B, w.bpre);
       B.bpre = w.bpre;
       B.bslots = c.h_scal[SC_BIGSLOTS];
@@ -894,14 +936,31 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       else k_big_rows<0><<<big_gx, 256, 0, g_bigs>>>(A, B);
       {
         const char *e = getenv("LTS_LEVEL_MIN");
-        g_level_min = e ? atoi(e) : -1;
+        g_level_min = e ? atoi(e) : 0;
+        e = getenv("LTS_LEVEL_RATIO");
+        g_level_ratio = e ? atoi(e) : 32;
       }
-      k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B, g_level_min);
+      LTS_CUDA(cudaMemsetAsync(w.scal + SC_BIGACT + 1, 0, sizeof(int), g_bigs));
+      k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B, g_level_min, g_level_ratio, w.scal + SC_BIGACT + 1);
+      if (getenv("LTS_LEVEL_VERBOSE")) {  // the largest regions: slots, local maxima, path chosen
+        int hb[4 * BST_W], hp[5];
+        const int m = std::min(nbig, 4);
+        cudaMemcpyAsync(hb, w.bst, sizeof(int) * BST_W * m, cudaMemcpyDeviceToHost, g_bigs);
+        cudaMemcpyAsync(hp, w.bpre, sizeof(int) * (m + 1), cudaMemcpyDeviceToHost, g_bigs);
+        cudaStreamSynchronize(g_bigs);
+        for (int i = 0; i < m; i++)
+          fprintf(stderr, "[lts] big region %d: k %d local maxima %d level %d\n", i, hp[i + 1] - hp[i],
+                  hb[i * BST_W + BST_NMAX], hb[i * BST_W + BST_LEVEL]);
+      }
       g_launches += 4;
-      // the level-parallel floods synchronise with the host: queue the main
-      // stream's work first (below) and run every iteration from the loop there
-      if (g_level_min < 0) LTS_TRY(big_iteration(c, A, B, big_gx));
-      else k_fill_int<<<1, 32, 0, g_bigs>>>(B.nactive, 1, 1);
+      // which regions flood level-parallel is decided on the device: one readback,
+      // then the first flood of every large region is queued before the main
+      // stream's work so the long floods start first
+      LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_BIGACT + 1, w.scal + SC_BIGACT + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                               g_bigs));
+      LTS_CUDA(cudaStreamSynchronize(g_bigs));
+      g_nlevel = c.h_scal[SC_BIGACT + 1];
+      LTS_TRY(big_iteration(c, A, B, big_gx));
     }
     A.qbase = nbig;
     if (R > nbig) {
