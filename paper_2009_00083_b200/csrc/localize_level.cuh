@@ -304,25 +304,81 @@ __device__ __forceinline__ void lv_jump(const LvArgs &L, int t0, int nt) {
   }
 }
 
-// beta: (smallest j on the tree path so far, ancestor reached)
-__device__ __forceinline__ void lv_pm_init(const LvArgs &L, int t0, int nt) {
-  LV_FOR(j, L) {
-    if (L.task[j] < 0) continue;
-    L.pm[j] = lv_pack((unsigned)j, (unsigned)L.par[j]);
-  }
-}
+// ---- beta of a level on the static tree -------------------------------------
+// The spanning forest R is built once per flood (level 1 graph: only the
+// region's source counts as +infinity) and never re-rooted: a class is a
+// connected piece of R, and the maximum spanning forest of a later task lies
+// inside R's edges plus the edges from the task's source set S to the class.
+// So beta(v) is a multi-source bottleneck on R restricted to the class:
+//     H(v) = max over pins z of min key on the R-path z..v,
+// pins = members adjacent to S.  Two sweeps of exact pointer doubling over the
+// parent pointers (segments [v, anc) with their minimum):
+//   up:   g(a) = max over pins z below a of pathmin(z..a)   (pushed, atomicMax)
+//   down: H(v) = max over ancestors a of min(g(a), pathmin(v..a))   (pulled)
+// max / min are idempotent, so the in-place updates of g need no ordering
+// beyond the barrier between rounds; the doubling tables are double-buffered.
+constexpr unsigned LV_NIL = 0xffffffffu;
 
-__device__ __forceinline__ void lv_pm_round(const LvArgs &L, int *changed, int t0, int nt) {
-  int ch = 0;
+template <int K>
+__device__ __forceinline__ void lv_pins(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, unsigned long long *J,
+                                        int t0, int nt) {
   LV_FOR(j, L) {
     const int tk = L.task[j];
     if (tk < 0) continue;
-    const unsigned long long a = L.pm[j];
-    const int anc = (int)(unsigned)(a & 0xffffffffu);
-    if (anc == tk) continue;
-    const unsigned long long b = L.pm[anc];
-    const unsigned m = min((unsigned)(a >> 32), (unsigned)(b >> 32));
-    L.pm[j] = lv_pack(m, (unsigned)(b & 0xffffffffu));
+    bool pin = L.sval[j] == tk;  // a source of an ascending flood (virtual root)
+    if (!pin) {
+      const LvRef R = lv_ref(A, Bg, j);
+      int q[K];
+      lv_load_row<K>(Bg, R, j, q);
+#pragma unroll
+      for (int kk = 0; kk < K; kk++) {
+        if (q[kk] < 0) continue;
+        const int u = R.jb + q[kk];
+        if (u == tk || (L.task[u] < 0 && L.sval[u] == tk)) pin = true;
+      }
+    }
+    L.comp[j] = pin ? j : -1;  // g, then H
+    L.csize[j] = 0;
+    const int pa = L.par[j];
+    const bool in = pa >= 0 && L.task[pa] == tk;
+    J[j] = lv_pack((unsigned)j, in ? (unsigned)pa : LV_NIL);
+  }
+}
+
+// segments for the second sweep
+__device__ __forceinline__ void lv_jinit(const LvArgs &L, unsigned long long *J, int t0, int nt) {
+  LV_FOR(j, L) {
+    const int tk = L.task[j];
+    if (tk < 0) continue;
+    const int pa = L.par[j];
+    const bool in = pa >= 0 && L.task[pa] == tk;
+    J[j] = lv_pack((unsigned)j, in ? (unsigned)pa : LV_NIL);
+  }
+}
+
+template <bool UP>
+__device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned long long *Jc, unsigned long long *Jn,
+                                               int *changed, int t0, int nt) {
+  int ch = 0;
+  int *g = L.comp;
+  LV_FOR(j, L) {
+    if (L.task[j] < 0) continue;
+    const unsigned long long a = Jc[j];
+    const unsigned anc = (unsigned)(a & 0xffffffffu);
+    if (anc == LV_NIL) {
+      Jn[j] = a;
+      continue;
+    }
+    const int pmin = (int)(a >> 32);  // smallest j in [j, anc)
+    if (UP) {
+      const int gv = g[j];
+      if (gv >= 0) atomicMax(g + anc, min(min(gv, pmin), (int)anc));
+    } else {
+      const int cand = min(pmin, g[anc]);
+      if (cand > g[j]) g[j] = cand;
+    }
+    const unsigned long long b = Jc[anc];
+    Jn[j] = lv_pack((unsigned)min(pmin, (int)(b >> 32)), (unsigned)(b & 0xffffffffu));
     ch = 1;
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
@@ -337,7 +393,7 @@ __device__ __forceinline__ void lv_classes(const LvArgs &L, int *active_ctr, int
     const int tk = j < L.nj ? L.task[j] : -1;
     int beta = -1;
     if (tk >= 0) {
-      beta = (int)(L.pm[j] >> 32);
+      beta = L.comp[j];
       if (beta == j) {
         L.fp[j] = (unsigned)L.skey[tk];
         L.lvl[j] = L.level;
@@ -441,8 +497,15 @@ template <int K>
 __global__ void __launch_bounds__(256) k_lv_scan(LocArgs A, BigArgs Bg, LvArgs L) { lv_scan<K>(A, Bg, L, LV_T0, LV_NT); }
 __global__ void __launch_bounds__(256) k_lv_hook(LvArgs L) { lv_hook(L, L.ctr + LVC_HOOKS, LV_T0, LV_NT); }
 __global__ void __launch_bounds__(256) k_lv_jump(LvArgs L) { lv_jump(L, LV_T0, LV_NT); }
-__global__ void __launch_bounds__(256) k_lv_pm_init(LvArgs L) { lv_pm_init(L, LV_T0, LV_NT); }
-__global__ void __launch_bounds__(256) k_lv_pm_round(LvArgs L) { lv_pm_round(L, L.ctr + LVC_CHANGED, LV_T0, LV_NT); }
+template <int K>
+__global__ void __launch_bounds__(256) k_lv_pins(LocArgs A, BigArgs Bg, LvArgs L, unsigned long long *J) {
+  lv_pins<K>(A, Bg, L, J, LV_T0, LV_NT);
+}
+__global__ void __launch_bounds__(256) k_lv_jinit(LvArgs L, unsigned long long *J) { lv_jinit(L, J, LV_T0, LV_NT); }
+template <bool UP>
+__global__ void __launch_bounds__(256) k_lv_sweep(LvArgs L, const unsigned long long *Jc, unsigned long long *Jn) {
+  lv_sweep_round<UP>(L, Jc, Jn, L.ctr + LVC_CHANGED, LV_T0, LV_NT);
+}
 __global__ void __launch_bounds__(256) k_lv_classes(LvArgs L) { lv_classes(L, L.ctr + LVC_ACTIVE, LV_T0, LV_NT); }
 __global__ void __launch_bounds__(256) k_lv_sortkeys(LvArgs L) { lv_sortkeys(L, LV_T0, LV_NT); }
 __global__ void __launch_bounds__(256) k_lv_gather(LvArgs L) { lv_gather(L, LV_T0, LV_NT); }
@@ -481,16 +544,10 @@ __global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L
   grid.sync();
   int active = *(volatile int *)(ctr + LVK_INIT);
   int rounds = 0, cslot = 0;
-  L.level = 0;
-  while (active > 0) {
-    L.level++;
-    const int apar = L.level & 1;
-    LV_TICK(7)
-    lv_chain<K>(A, Bg, L, t0, nt);
-    grid.sync();
-    LV_TICK(0)
+  // the spanning forest R of the whole flood, rooted at the sources
+  if (active > 0) {
+    L.level = 1;
     lv_prep(L, t0, nt);
-    if (lead) ctr[LVK_ACTIVE + apar] = 0;
     grid.sync();
     LV_TICK(1)
     for (int round = 0; round < 64; round++, rounds++) {
@@ -508,14 +565,35 @@ __global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L
       LV_TICK(4)
       if (h == 0) break;
     }
-    lv_pm_init(L, t0, nt);
+  }
+  L.level = 0;
+  unsigned long long *Ja = L.pm, *Jb = L.best;
+  while (active > 0) {
+    L.level++;
+    const int apar = L.level & 1;
+    lv_chain<K>(A, Bg, L, t0, nt);
     grid.sync();
-    for (int it = 0; it < 64; it++) {
-      cslot = cslot == 2 ? 0 : cslot + 1;
-      if (lead) ctr[LVK_CHANGED + (cslot == 2 ? 0 : cslot + 1)] = 0;
-      lv_pm_round(L, ctr + LVK_CHANGED + cslot, t0, nt);
-      grid.sync();
-      if (*(volatile int *)(ctr + LVK_CHANGED + cslot) == 0) break;
+    LV_TICK(0)
+    lv_pins<K>(A, Bg, L, Ja, t0, nt);
+    if (lead) ctr[LVK_ACTIVE + apar] = 0;
+    grid.sync();
+    for (int sweep = 0; sweep < 2; sweep++) {
+      unsigned long long *Jc = Ja, *Jn = Jb;
+      for (int it = 0; it < 40; it++) {
+        cslot = cslot == 2 ? 0 : cslot + 1;
+        if (lead) ctr[LVK_CHANGED + (cslot == 2 ? 0 : cslot + 1)] = 0;
+        if (sweep == 0) lv_sweep_round<true>(L, Jc, Jn, ctr + LVK_CHANGED + cslot, t0, nt);
+        else lv_sweep_round<false>(L, Jc, Jn, ctr + LVK_CHANGED + cslot, t0, nt);
+        grid.sync();
+        unsigned long long *tmp = Jc;
+        Jc = Jn;
+        Jn = tmp;
+        if (*(volatile int *)(ctr + LVK_CHANGED + cslot) == 0) break;
+      }
+      if (sweep == 0) {
+        lv_jinit(L, Ja, t0, nt);
+        grid.sync();
+      }
     }
     LV_TICK(5)
     lv_classes(L, ctr + LVK_ACTIVE + apar, t0, nt);

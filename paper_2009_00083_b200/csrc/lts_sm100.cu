@@ -660,13 +660,10 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
     g_launches += 2;
     LTS_TRY(lv_read(c, LVC_ACTIVE, 1));
     int active = hc[LVC_ACTIVE];
-    while (active > 0) {
-      L.level = ++levels;
-      if (nd == 2) k_lv_chain<6><<<gj, 256, 0, s>>>(A, B, L);
-      else if (nd == 3) k_lv_chain<14><<<gj, 256, 0, s>>>(A, B, L);
-      else k_lv_chain<kCsrK><<<gj, 256, 0, s>>>(A, B, L);
+    if (active > 0) {  // the spanning forest of the flood
+      L.level = 1;
       k_lv_prep<<<gj, 256, 0, s>>>(L);
-      g_launches += 2;
+      g_launches++;
       for (int round = 0;; round++) {
         if (round >= 64) return lts_set_error(LTS_E_CUDA, "level flood: spanning forest did not converge");
         LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_HOOKS, 0, sizeof(int), s));
@@ -680,16 +677,32 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
         LTS_TRY(lv_read(c, LVC_HOOKS, 1));
         if (hc[LVC_HOOKS] == 0) break;
       }
-      k_lv_pm_init<<<gj, 256, 0, s>>>(L);
-      g_launches++;
-      for (int it = 0;; it++) {
-        if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: path minima did not converge");
-        LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
-        k_lv_pm_round<<<gj, 256, 0, s>>>(L);
-        k_lv_pm_round<<<gj, 256, 0, s>>>(L);
-        g_launches += 2;
-        LTS_TRY(lv_read(c, LVC_CHANGED, 1));
-        if (hc[LVC_CHANGED] == 0) break;
+    }
+    while (active > 0) {
+      L.level = ++levels;
+      if (nd == 2) k_lv_chain<6><<<gj, 256, 0, s>>>(A, B, L);
+      else if (nd == 3) k_lv_chain<14><<<gj, 256, 0, s>>>(A, B, L);
+      else k_lv_chain<kCsrK><<<gj, 256, 0, s>>>(A, B, L);
+      if (nd == 2) k_lv_pins<6><<<gj, 256, 0, s>>>(A, B, L, L.pm);
+      else if (nd == 3) k_lv_pins<14><<<gj, 256, 0, s>>>(A, B, L, L.pm);
+      else k_lv_pins<kCsrK><<<gj, 256, 0, s>>>(A, B, L, L.pm);
+      g_launches += 2;
+      for (int sweep = 0; sweep < 2; sweep++) {
+        unsigned long long *Jc = L.pm, *Jn = L.best;
+        for (int it = 0;; it++) {
+          if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: sweep did not converge");
+          LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
+          if (sweep == 0) k_lv_sweep<true><<<gj, 256, 0, s>>>(L, Jc, Jn);
+          else k_lv_sweep<false><<<gj, 256, 0, s>>>(L, Jc, Jn);
+          g_launches++;
+          std::swap(Jc, Jn);
+          LTS_TRY(lv_read(c, LVC_CHANGED, 1));
+          if (hc[LVC_CHANGED] == 0) break;
+        }
+        if (sweep == 0) {
+          k_lv_jinit<<<gj, 256, 0, s>>>(L, L.pm);
+          g_launches++;
+        }
       }
       LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_ACTIVE, 0, sizeof(int), s));
       k_lv_classes<<<gj, 256, 0, s>>>(L);
