@@ -46,6 +46,10 @@ constexpr int BIG_SMEM_WORDS = 16 * 1024;     // bit-set words in shared memory 
 #endif
 constexpr int BIG_THRESHOLD = LTS_BIG_THRESHOLD;  // regions with k > this use this kernel
 
+#ifndef LTS_LEVEL_NMAX
+#define LTS_LEVEL_NMAX 256
+#endif
+
 struct BigArgs {
   int *v0;           // per big region: first admissible boundary minimum
   int *inv;          // key -> local index, S + R entries (region base lo + rid)
@@ -818,7 +822,7 @@ __device__ __forceinline__ BigRef big_ref(const LocArgs &A, const BigArgs &Bg, i
 }
 
 // per region: v0 from k_big_rows; no admissible minimum -> status 1
-__global__ void k_big_init(LocArgs A, BigArgs Bg, int level_min, int level_ratio, int *nlevel) {
+__global__ void k_big_init(LocArgs A, BigArgs Bg, int level_min, int level_ratio, int level_giant, int *nlevel) {
   GRID_STRIDE(qi, Bg.nbig) {
     const BigRef R = big_ref(A, Bg, (int)qi);
     const int v0 = Bg.v0[qi];
@@ -827,8 +831,12 @@ __global__ void k_big_init(LocArgs A, BigArgs Bg, int level_min, int level_ratio
     st[BST_BAD] = 0;
     st[BST_DIFF] = 0;
     st[BST_NSRC] = 0;
-    // rough regions (many local maxima per vertex) flood level-parallel
-    const int lev = level_min >= 0 && R.k >= level_min && (long long)st[BST_NMAX] * level_ratio >= R.k ? 1 : 0;
+    // rough regions flood level-parallel (many local maxima per vertex, or many
+    // in absolute terms: the CTA flood needs about one step per ascent), and
+    // so do the regions whose bit sets would not fit its shared memory
+    const int nmax = st[BST_NMAX];
+    const int lev = level_min >= 0 && R.k >= level_min &&
+                    ((long long)nmax * level_ratio >= R.k || nmax >= LTS_LEVEL_NMAX || R.k >= level_giant) ? 1 : 0;
     st[BST_LEVEL] = lev;
     if (lev) atomicAdd(nlevel, 1);
     if (v0 == 0x7fffffff) {

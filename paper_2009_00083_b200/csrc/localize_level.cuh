@@ -62,6 +62,8 @@ struct LvArgs {
   int *ctr;
   int nj;
   int level;
+  const int *alist;  // vertices still active at this level (nullptr: scan the whole key space)
+  int na;
 };
 
 struct LvRef {
@@ -97,6 +99,10 @@ __device__ __forceinline__ unsigned long long lv_pack(unsigned hi, unsigned lo) 
 // a kernel of its own on the host-driven path, a stage between grid barriers
 // in the cooperative kernel.
 #define LV_FOR(j, L) for (int j = t0; j < (L).nj; j += nt)
+// over the level's active list
+#define LV_ACT(j, L)                                                                    \
+  for (int i_ = t0, j = 0, lim_ = (L).alist ? (L).na : (L).nj;                          \
+       i_ < lim_ && ((j = (L).alist ? (L).alist[i_] : i_), true); i_ += nt)
 
 template <int K>
 __device__ __forceinline__ void lv_load_row(const BigArgs &Bg, const LvRef &R, int j, int (&q)[K]) {
@@ -170,8 +176,11 @@ __device__ __forceinline__ void lv_init(const LocArgs &A, const BigArgs &Bg, con
 // of z(i+1) is z(i), and the rest of the task floods from the sources
 // {p, z1, .., zm} together (they all count as +infinity).  One thread per task.
 template <int K>
-__device__ __forceinline__ void lv_chain(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, int t0, int nt) {
-  LV_FOR(p, L) {
+__device__ __forceinline__ void lv_chain(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, const int *plist,
+                                         int np, int t0, int nt) {
+  // candidates: the vertices active at the previous level (plist), or every key
+  for (int i_ = t0, lim_ = plist ? np : L.nj; i_ < lim_; i_ += nt) {
+    const int p = plist ? plist[i_] : i_;
     if (L.lvl[p] != L.level - 1 || L.csize[p] <= 1 || L.task[p] != LV_DONE) continue;
     const LvRef R = lv_ref(A, Bg, p);
     int cur = p, last = -1;
@@ -322,7 +331,7 @@ constexpr unsigned LV_NIL = 0xffffffffu;
 template <int K>
 __device__ __forceinline__ void lv_pins(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, unsigned long long *J,
                                         int t0, int nt) {
-  LV_FOR(j, L) {
+  LV_ACT(j, L) {
     const int tk = L.task[j];
     if (tk < 0) continue;
     bool pin = L.sval[j] == tk;  // a source of an ascending flood (virtual root)
@@ -347,7 +356,7 @@ __device__ __forceinline__ void lv_pins(const LocArgs &A, const BigArgs &Bg, con
 
 // segments for the second sweep
 __device__ __forceinline__ void lv_jinit(const LvArgs &L, unsigned long long *J, int t0, int nt) {
-  LV_FOR(j, L) {
+  LV_ACT(j, L) {
     const int tk = L.task[j];
     if (tk < 0) continue;
     const int pa = L.par[j];
@@ -361,7 +370,7 @@ __device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned l
                                                int *changed, int t0, int nt) {
   int ch = 0;
   int *g = L.comp;
-  LV_FOR(j, L) {
+  LV_ACT(j, L) {
     if (L.task[j] < 0) continue;
     const unsigned long long a = Jc[j];
     const unsigned anc = (unsigned)(a & 0xffffffffu);
@@ -388,9 +397,11 @@ __device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned l
 // task source's chain), the others join the task of their class's trunk vertex
 __device__ __forceinline__ void lv_classes(const LvArgs &L, int *active_ctr, int t0, int nt) {
   int act = 0;
-  for (int j0 = t0 - (int)(threadIdx.x & 31); j0 < L.nj; j0 += nt) {
-    const int j = j0 + (threadIdx.x & 31);
-    const int tk = j < L.nj ? L.task[j] : -1;
+  const int lim = L.alist ? L.na : L.nj;
+  for (int i0 = t0 - (int)(threadIdx.x & 31); i0 < lim; i0 += nt) {
+    const int i = i0 + (threadIdx.x & 31);
+    const int j = i < lim ? (L.alist ? L.alist[i] : i) : -1;
+    const int tk = j >= 0 ? L.task[j] : -1;
     int beta = -1;
     if (tk >= 0) {
       beta = L.comp[j];
@@ -407,8 +418,37 @@ __device__ __forceinline__ void lv_classes(const LvArgs &L, int *active_ctr, int
     const unsigned peers = __match_any_sync(0xffffffffu, beta);
     if (beta >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(L.csize + beta, __popc(peers));
   }
-  act = __reduce_add_sync(0xffffffffu, act);
-  if ((threadIdx.x & 31) == 0 && act) atomicAdd(active_ctr, act);
+  if (active_ctr) {
+    act = __reduce_add_sync(0xffffffffu, act);
+    if ((threadIdx.x & 31) == 0 && act) atomicAdd(active_ctr, act);
+  }
+}
+
+// the active list of the next level, in key order within a block's tile so
+// the phases that follow stay coalesced; *cursor ends as the active count
+__device__ __forceinline__ void lv_build_list(const LvArgs &L, int *list, int *cursor) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int tile = blockIdx.x * blockDim.x; tile < L.nj; tile += gridDim.x * blockDim.x) {
+    const int j = tile + threadIdx.x;
+    const bool on = j < L.nj && L.task[j] >= 0;
+    const unsigned m = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) wsum[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < nw; w++) {
+        const int c = wsum[w];
+        wsum[w] = tot;
+        tot += c;
+      }
+      base = tot ? atomicAdd(cursor, tot) : 0;
+    }
+    __syncthreads();
+    if (on) list[base + wsum[warp] + __popc(m & lanemask_lt())] = j;
+    __syncthreads();
+  }
 }
 
 // ---- extraction indices: preorder of F, children in decreasing key ----------
@@ -491,7 +531,9 @@ __global__ void __launch_bounds__(256) k_lv_init(LocArgs A, BigArgs Bg, LvArgs L
   lv_init(A, Bg, L, L.ctr + LVC_ACTIVE, LV_T0, LV_NT);
 }
 template <int K>
-__global__ void __launch_bounds__(256) k_lv_chain(LocArgs A, BigArgs Bg, LvArgs L) { lv_chain<K>(A, Bg, L, LV_T0, LV_NT); }
+__global__ void __launch_bounds__(256) k_lv_chain(LocArgs A, BigArgs Bg, LvArgs L) {
+  lv_chain<K>(A, Bg, L, nullptr, 0, LV_T0, LV_NT);
+}
 __global__ void __launch_bounds__(256) k_lv_prep(LvArgs L) { lv_prep(L, LV_T0, LV_NT); }
 template <int K>
 __global__ void __launch_bounds__(256) k_lv_scan(LocArgs A, BigArgs Bg, LvArgs L) { lv_scan<K>(A, Bg, L, LV_T0, LV_NT); }
@@ -568,10 +610,19 @@ __global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L
   }
   L.level = 0;
   unsigned long long *Ja = L.pm, *Jb = L.best;
+  // The active list of a level is built at the end of the previous one, the
+  // two buffers (link, oval: both free once the forest stands) alternating;
+  // level 1 runs over the whole key space.  The list a level ran over holds
+  // the trunk vertices it placed: the chain candidates of the next level.
+  int *bufs[2] = {L.link, L.oval};
+  const int *plist = nullptr;
+  int np = 0;
+  L.alist = nullptr;
+  L.na = active;
   while (active > 0) {
     L.level++;
     const int apar = L.level & 1;
-    lv_chain<K>(A, Bg, L, t0, nt);
+    lv_chain<K>(A, Bg, L, plist, np, t0, nt);
     grid.sync();
     LV_TICK(0)
     lv_pins<K>(A, Bg, L, Ja, t0, nt);
@@ -596,10 +647,17 @@ __global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L
       }
     }
     LV_TICK(5)
-    lv_classes(L, ctr + LVK_ACTIVE + apar, t0, nt);
+    lv_classes(L, nullptr, t0, nt);
+    grid.sync();
+    int *lnext = bufs[apar];
+    lv_build_list(L, lnext, ctr + LVK_ACTIVE + apar);
     grid.sync();
     LV_TICK(6)
     active = *(volatile int *)(ctr + LVK_ACTIVE + apar);
+    plist = L.alist;
+    np = L.na;
+    L.alist = lnext;
+    L.na = active;
   }
   if (lead) {
     ctr[LVK_LEVELS] = L.level;

@@ -558,11 +558,14 @@ static int big_stream_join(cudaStream_t s) {
 // one CTA per region for the flood, grid-wide checks, per-region decision
 static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B);
 // Flood policy: a large region floods level-parallel (localize_level.cuh) when it
-// is rough, i.e. has at least k / ratio local maxima in its initial order; smooth
-// regions keep the batched CTA flood (their level count grows with the length
-// of the climb).  LTS_LEVEL_MIN=-1 disables the level path, LTS_LEVEL_RATIO
-// moves the threshold.
-static int g_level_min = 0, g_level_ratio = 32;
+// is rough, i.e. has at least k / ratio local maxima in its initial order, or
+// when it has at least `giant` slots (its bit sets would spill out of the CTA
+// flood's shared memory).  Small smooth regions keep the batched CTA flood: it
+// commits long monotone runs per step, while the level count of the level
+// path grows with the number of bumps on the climb from the saddle.
+// LTS_LEVEL_MIN=-1 disables the level path; LTS_LEVEL_RATIO / LTS_LEVEL_GIANT
+// move the thresholds.
+static int g_level_min = 0, g_level_ratio = 32, g_level_giant = 32 * BIG_SMEM_WORDS;
 static int g_nlevel = 0;  // level-flooded regions of the current pass
 
 static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
@@ -626,6 +629,8 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
   L.ctr = w.scal + SC_LV;
   L.nj = B.bslots + B.nbig;
   L.level = 0;
+  L.alist = nullptr;
+  L.na = 0;
   cudaStream_t s = g_lvs;
   const int gj = (int)std::min<int64_t>(((int64_t)L.nj + 255) / 256, 148 * 8);
   const int gs = (int)std::min<int64_t>(((int64_t)B.bslots + 255) / 256, 148 * 8);
@@ -952,9 +957,11 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         g_level_min = e ? atoi(e) : 0;
         e = getenv("LTS_LEVEL_RATIO");
         g_level_ratio = e ? atoi(e) : 32;
+        e = getenv("LTS_LEVEL_GIANT");
+        g_level_giant = e ? atoi(e) : 32 * BIG_SMEM_WORDS;
       }
       LTS_CUDA(cudaMemsetAsync(w.scal + SC_BIGACT + 1, 0, sizeof(int), g_bigs));
-      k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B, g_level_min, g_level_ratio, w.scal + SC_BIGACT + 1);
+      k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B, g_level_min, g_level_ratio, g_level_giant, w.scal + SC_BIGACT + 1);
       if (getenv("LTS_LEVEL_VERBOSE")) {  // the largest regions: slots, local maxima, path chosen
         int hb[4 * BST_W], hp[5];
         const int m = std::min(nbig, 4);
