@@ -206,6 +206,86 @@ __device__ __forceinline__ void lv_chain(const LocArgs &A, const BigArgs &Bg, co
   }
 }
 
+// Flood prefix (cooperative path).  Any prefix of a task's exact extraction
+// order can be placed up front as a chain in F, the rest of the task flooding
+// from the source plus that prefix.  One warp per task source runs the plain
+// priority flood with its frontier in shared memory: as long as it climbs
+// (every step of an ascent is free: the chain rule above), and otherwise for a
+// budget of steps proportional to the task's size, so that the sequential
+// prefix costs about as much as the level's sweeps over the task.  On a climb
+// through a bumpy field a level then crosses many bumps instead of one.
+constexpr int LV_FCAP = 704;    // frontier entries per warp (static shared memory: 16 x 704 ints)
+constexpr int LV_WARPS = 16;    // warps per block of the cooperative kernel
+
+__device__ __forceinline__ void lv_sources(const LvArgs &L, const int *plist, int np, int *srclist, int *nsrc,
+                                           int t0, int nt) {
+  for (int i_ = t0, lim_ = plist ? np : L.nj; i_ < lim_; i_ += nt) {
+    const int p = plist ? plist[i_] : i_;
+    if (L.lvl[p] != L.level - 1 || L.csize[p] <= 1 || L.task[p] != LV_DONE) continue;
+    srclist[atomicAdd(nsrc, 1)] = p;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void lv_prefix(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, const int *srclist,
+                                          int ns, int (*fr_all)[LV_FCAP], int t0, int nt) {
+  static_assert(K <= 32, "one lane per neighbour slot");
+  const int lane = threadIdx.x & 31;
+  int *fr = fr_all[threadIdx.x >> 5];
+  const int mark = -(3 + L.level);  // "in the frontier of this level's prefix"
+  for (int si = t0 >> 5; si < ns; si += nt >> 5) {
+    const int p = srclist[si];
+    const LvRef R = lv_ref(A, Bg, p);
+    const int budget = min(4096, L.csize[p] >> 13);
+    int nf = 0, cur = p, last = -1, prev = p, steps = 0;
+    for (;;) {
+      // the unplaced member neighbours of the vertex just placed join the frontier
+      int u = -1;
+      if (lane < K) {
+        const int q = Bg.nrowkey[((size_t)R.lo + R.rid + (cur - R.jb)) * K + lane];
+        if (q >= 0) {
+          u = R.jb + q;
+          if (L.task[u] != p || L.lvl[u] == mark) u = -1;
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, u >= 0);
+      if (u >= 0) {
+        L.lvl[u] = mark;
+        fr[nf + __popc(m & lanemask_lt())] = u;
+      }
+      nf += __popc(m);
+      __syncwarp();
+      if (nf == 0) break;
+      int best = -1, bi = 0;
+      for (int i = lane; i < nf; i += 32) {
+        const int x = fr[i];
+        if (x > best) {
+          best = x;
+          bi = i;
+        }
+      }
+      const int z = __reduce_max_sync(0xffffffffu, best);
+      if (z < last && steps >= budget) break;
+      if (nf - 1 + K > LV_FCAP) break;  // no room for the next vertex's neighbours
+      const unsigned own = __ballot_sync(0xffffffffu, best == z);
+      bi = __shfl_sync(0xffffffffu, bi, __ffs(own) - 1);
+      if (lane == 0) {
+        fr[bi] = fr[nf - 1];
+        L.task[z] = LV_DONE;
+        L.fp[z] = (unsigned)prev;
+        L.lvl[z] = L.level;
+        L.csize[z] = 1;
+        L.sval[z] = p;
+      }
+      nf--;
+      __syncwarp();
+      prev = last = cur = z;
+      steps++;
+    }
+    if (lane == 0) L.skey[p] = prev;
+  }
+}
+
 // per level: singleton components, no tree edges; the sources of an ascending
 // flood start inside the (virtual) root's component
 __device__ __forceinline__ void lv_prep(const LvArgs &L, int t0, int nt) {
@@ -562,7 +642,7 @@ __global__ void __launch_bounds__(256) k_lv_write(LocArgs A, BigArgs Bg, LvArgs 
 // the hook counter alternates between two slots (read before the round's last
 // barrier), the changed flag rotates over three (read after its barrier), the
 // active count alternates by level.
-enum { LVK_HOOKS = 0, LVK_CHANGED = 2, LVK_ACTIVE = 5, LVK_INIT = 7, LVK_LEVELS = 8, LVK_ROUNDS = 9 };
+enum { LVK_HOOKS = 0, LVK_CHANGED = 2, LVK_ACTIVE = 5, LVK_INIT = 7, LVK_LEVELS = 8, LVK_ROUNDS = 9, LVK_NSRC = 10 };
 
 // phase clocks of the lead thread (LTS_LEVEL_VERBOSE): chain, prep, scan, hook, jump, beta, classes
 __device__ long long d_lvclk[8];
@@ -574,8 +654,9 @@ __device__ long long d_lvclk[8];
   }
 
 template <int K>
-__global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L) {
+__global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ int s_front[LV_WARPS][LV_FCAP];
   const int t0 = LV_T0, nt = LV_NT;
   const bool lead = t0 == 0;
   long long tq = clock64();
@@ -622,11 +703,16 @@ __global__ void __launch_bounds__(512) k_lv_coop(LocArgs A, BigArgs Bg, LvArgs L
   while (active > 0) {
     L.level++;
     const int apar = L.level & 1;
-    lv_chain<K>(A, Bg, L, plist, np, t0, nt);
+    lv_sources(L, plist, np, (int *)Jb, ctr + LVK_NSRC + apar, t0, nt);
+    grid.sync();
+    lv_prefix<K>(A, Bg, L, (const int *)Jb, *(volatile int *)(ctr + LVK_NSRC + apar), s_front, t0, nt);
     grid.sync();
     LV_TICK(0)
     lv_pins<K>(A, Bg, L, Ja, t0, nt);
-    if (lead) ctr[LVK_ACTIVE + apar] = 0;
+    if (lead) {
+      ctr[LVK_ACTIVE + apar] = 0;
+      ctr[LVK_NSRC + (apar ^ 1)] = 0;
+    }
     grid.sync();
     for (int sweep = 0; sweep < 2; sweep++) {
       unsigned long long *Jc = Ja, *Jn = Jb;
