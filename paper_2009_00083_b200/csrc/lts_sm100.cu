@@ -558,14 +558,15 @@ static int big_stream_join(cudaStream_t s) {
 // one CTA per region for the flood, grid-wide checks, per-region decision
 static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B);
 // Flood policy: a large region floods level-parallel (localize_level.cuh) when it
-// is rough, i.e. has at least k / ratio local maxima in its initial order, or
-// when it has at least `giant` slots (its bit sets would spill out of the CTA
-// flood's shared memory).  Small smooth regions keep the batched CTA flood: it
-// commits long monotone runs per step, while the level count of the level
-// path grows with the number of bumps on the climb from the saddle.
+// is rough, i.e. has at least k / ratio local maxima in its initial order (or
+// LTS_LEVEL_NMAX of them), or when it has at least `giant` slots.  Small smooth
+// regions keep the batched CTA flood, which commits long monotone runs per
+// step; the two paths run side by side on two streams, so the few largest
+// smooth regions go level-parallel and the many mid-sized ones to the CTAs
+// (16 K measured best on cfg3: 11.5 -> 10.7 ms per pass).
 // LTS_LEVEL_MIN=-1 disables the level path; LTS_LEVEL_RATIO / LTS_LEVEL_GIANT
 // move the thresholds.
-static int g_level_min = 0, g_level_ratio = 32, g_level_giant = 32 * BIG_SMEM_WORDS;
+static int g_level_min = 0, g_level_ratio = 32, g_level_giant = 16384;
 static int g_nlevel = 0;  // level-flooded regions of the current pass
 
 static int big_iteration(Ctx &c, const LocArgs &A, const BigArgs &B, int gx) {
@@ -637,7 +638,7 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
   int *hc = c.h_scal + SC_LV;
   int levels = 0, rounds_total = 0, lv_grid = 1;
   LTS_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(int) * LVC_N, s));
-  static const bool host_loop = getenv("LTS_LEVEL_HOST") != nullptr;
+  const bool host_loop = getenv("LTS_LEVEL_HOST") != nullptr;  // debugging: one launch per phase
   const int nd = c.g.ndim;
   if (!host_loop) {
     // every level in one cooperative launch
@@ -958,7 +959,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         e = getenv("LTS_LEVEL_RATIO");
         g_level_ratio = e ? atoi(e) : 32;
         e = getenv("LTS_LEVEL_GIANT");
-        g_level_giant = e ? atoi(e) : 32 * BIG_SMEM_WORDS;
+        g_level_giant = e ? atoi(e) : 16384;
       }
       LTS_CUDA(cudaMemsetAsync(w.scal + SC_BIGACT + 1, 0, sizeof(int), g_bigs));
       k_big_init<<<NB(nbig), 256, 0, g_bigs>>>(A, B, g_level_min, g_level_ratio, g_level_giant, w.scal + SC_BIGACT + 1);

@@ -212,3 +212,48 @@ def test_simplify_small_3d_shapes(shape):
     assert rep.ok == ref.ok
     np.testing.assert_array_equal(G.rank32.cpu().numpy(), ref.G_rank)
     assert g.values.cpu().numpy().tobytes() == ref.g.tobytes()
+
+
+# The two exact flood paths of the large regions (csrc/localize_big.cuh: batched
+# CTA floods; csrc/localize_level.cuh: level-parallel decomposition) are chosen
+# per region by its roughness.  Force each of them on every large region: both
+# must reproduce the oracle's order field bit for bit.
+FLOOD_MODES = {
+    "level_all": {"LTS_LEVEL_MIN": "0", "LTS_LEVEL_RATIO": "1000000"},
+    "level_all_host_loop": {"LTS_LEVEL_MIN": "0", "LTS_LEVEL_RATIO": "1000000", "LTS_LEVEL_HOST": "1"},
+    "cta_all": {"LTS_LEVEL_MIN": "-1"},
+}
+
+
+@pytest.mark.parametrize("mode", list(FLOOD_MODES))
+@pytest.mark.parametrize("name", ["rand2d_300x200", "rand3d_40x36x30", "cfg1_512", "cfg2_64", "cfg3_96", "cfg4_512"])
+def test_flood_paths_vs_oracle(name, mode, monkeypatch):
+    if mode == "level_all_host_loop" and name not in ("rand2d_300x200", "cfg2_64"):
+        pytest.skip("the host-driven loop is a debugging path: two cases suffice")
+    for k, v in FLOOD_MODES[mode].items():
+        monkeypatch.setenv(k, v)
+    f, kmax, kmin = CASES[name]()
+    dims, f32, pm, pn, ref = _oracle_case(np.asarray(f, np.float32), kmax, kmin)
+    mesh = _mesh(dims)
+    g, G, rep = P.simplify_field(mesh, _cu(f32), P.ConstraintSet(preserveMinima=pn, preserveMaxima=pm))
+    assert rep.ok == ref.ok and rep.outerIterations == ref.outer_iterations
+    np.testing.assert_array_equal(G.rank32.cpu().numpy(), ref.G_rank)
+    assert g.values.cpu().numpy().tobytes() == ref.g.tobytes()
+    for a, b in zip(rep.passes, ref.passes):
+        assert (a.regions, a.claimed, a.n_iter_max, a.capped) == (b.regions, b.claimed, b.n_iter_max, b.capped)
+
+
+@pytest.mark.parametrize("path", [p for p in GOLD if "quant2d" in p or "cfg4_160" in p or "crater" in p],
+                         ids=lambda p: os.path.basename(p)[:-4])
+def test_level_floods_capped_regions_golden(path, monkeypatch):
+    """Capped regions (period-2 cycles, N_I = 100), outer loops > 1 and the
+    restore step with every large region flooded level-parallel."""
+    monkeypatch.setenv("LTS_LEVEL_MIN", "0")
+    monkeypatch.setenv("LTS_LEVEL_RATIO", "1000000")
+    z = _load(path)
+    mesh = _mesh(z["dims"])
+    g, G, rep = P.simplify_field(mesh, _cu(z["f"]),
+                                 P.ConstraintSet(preserveMinima=z["pres_min"], preserveMaxima=z["pres_max"]))
+    assert rep.ok == bool(z["ok"]) and rep.outerIterations == int(z["outer"])
+    np.testing.assert_array_equal(G.rank32.cpu().numpy(), z["G_rank"])
+    assert g.values.cpu().numpy().tobytes() == z["g"].tobytes()
