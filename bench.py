@@ -395,10 +395,12 @@ def main():
                             "frac": 9.0 * n / (clsptr_ms * 1e-3) / 1e9 / hbm,
                             "traffic": traffic.get("classify_ascent")},
     }
-    # dominant kernel: the large-region flood (k_big_flood), timed by the
-    # library with CUDA events on the stream it runs on.  Algorithmic bytes per
-    # flooded region slot: its neighbour-key row (4 K B), its key -> index
-    # entry (4 B) and its label (4 B); DESIGN.md section 4.
+    # dominant kernels: the large-region floods (k_big_flood for the smooth
+    # mid-sized regions beside k_lv_coop, the level-parallel floods of the rough
+    # and the largest regions), timed together by the library with CUDA events
+    # on the streams they run on.  Algorithmic bytes per flooded region slot:
+    # its neighbour-key row (4 K B), its key -> index entry (4 B) and its label
+    # (4 B); DESIGN.md section 4.
     K = 14 if mesh.dim == 3 else 6
     flood_ms = float(rep.phase_ms[9])
     flood_launches = int(rep.phase_ms[N.PH_FLOOD_LAUNCHES])
@@ -406,14 +408,15 @@ def main():
     per_launch_ms = flood_ms / max(flood_launches, 1)
     flood_bytes = (4.0 * K + 8.0) * flood_slots / max(flood_launches, 1)
     flood_gbs = flood_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0
-    roofline = {"bound": "hbm", "kernel": "k_big_flood", "achieved": flood_gbs, "peak": hbm,
+    roofline = {"bound": "hbm", "kernel": "k_big_flood || k_lv_coop", "achieved": flood_gbs, "peak": hbm,
                 "unit": "GB/s", "frac": flood_gbs / hbm, "traffic": traffic.get("k_big_flood"),
                 "peak_source": peak_kind, "launches": flood_launches, "ms_per_launch": per_launch_ms,
                 "bytes_per_launch": flood_bytes,
                 "share_of_step": flood_ms / phases["total"] if phases["total"] else None,
                 "slots_per_s": flood_slots / (flood_ms * 1e-3) if flood_ms > 0 else None,
-                "note": "latency-bound priority floods (one CTA per region, about one L2 round "
-                        "trip and five barriers per batched step); DESIGN.md section 4"}
+                "note": "latency-bound exact priority floods: one CTA per smooth region (about one L2 "
+                        "round trip and five barriers per batched step) beside the level-parallel "
+                        "decomposition (one grid barrier per phase); DESIGN.md section 4a"}
 
     # ---- end to end through the public API with host buffers ---------------
     g_host = torch.empty(n, dtype=torch.float32).pin_memory()
