@@ -434,25 +434,25 @@ __device__ __forceinline__ void lv_pins(const LocArgs &A, const BigArgs &Bg, con
   }
 }
 
-// segments for the second sweep
-__device__ __forceinline__ void lv_jinit(const LvArgs &L, unsigned long long *J, int t0, int nt) {
-  LV_ACT(j, L) {
-    const int tk = L.task[j];
-    if (tk < 0) continue;
-    const int pa = L.par[j];
-    const bool in = pa >= 0 && L.task[pa] == tk;
-    J[j] = lv_pack((unsigned)j, in ? (unsigned)pa : LV_NIL);
-  }
+// the doubling pair of j before any jump: ([j, parent), parent), parent NIL outside the task
+__device__ __forceinline__ unsigned long long lv_j0(const LvArgs &L, int j, int tk) {
+  const int pa = L.par[j];
+  const bool in = pa >= 0 && L.task[pa] == tk;
+  return lv_pack((unsigned)j, in ? (unsigned)pa : LV_NIL);
 }
 
-template <bool UP>
+// One doubling round.  FIRST: the pairs are read from the parent pointers (the
+// downward sweep restarts the doubling without an initialisation phase).  The
+// round reports whether any vertex still has an ancestor to jump to.
+template <bool UP, bool FIRST>
 __device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned long long *Jc, unsigned long long *Jn,
                                                int *changed, int t0, int nt) {
   int ch = 0;
   int *g = L.comp;
   LV_ACT(j, L) {
-    if (L.task[j] < 0) continue;
-    const unsigned long long a = Jc[j];
+    const int tk = L.task[j];
+    if (tk < 0) continue;
+    const unsigned long long a = FIRST ? lv_j0(L, j, tk) : Jc[j];
     const unsigned anc = (unsigned)(a & 0xffffffffu);
     if (anc == LV_NIL) {
       Jn[j] = a;
@@ -466,9 +466,9 @@ __device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned l
       const int cand = min(pmin, g[anc]);
       if (cand > g[j]) g[j] = cand;
     }
-    const unsigned long long b = Jc[anc];
+    const unsigned long long b = FIRST ? lv_j0(L, (int)anc, tk) : Jc[anc];
     Jn[j] = lv_pack((unsigned)min(pmin, (int)(b >> 32)), (unsigned)(b & 0xffffffffu));
-    ch = 1;
+    if ((unsigned)(b & 0xffffffffu) != LV_NIL) ch = 1;
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
@@ -504,18 +504,53 @@ __device__ __forceinline__ void lv_classes(const LvArgs &L, int *active_ctr, int
   }
 }
 
-// the active list of the next level, in key order within a block's tile so
-// the phases that follow stay coalesced; *cursor ends as the active count
-__device__ __forceinline__ void lv_build_list(const LvArgs &L, int *list, int *cursor) {
-  __shared__ int wsum[32];
+// classes and the active list of the next level in one phase (cooperative
+// path): a block takes tiles of the current list (level 1: of the key space),
+// and the vertices still unplaced are appended tile by tile, in order, so the
+// phases that follow stay coalesced; *cursor ends as the active count
+__device__ __forceinline__ void lv_classes_list(const LvArgs &L, int *list, int *cursor) {
+  __shared__ int wsum[32], wbeta[32], wcnt[32];
   __shared__ int base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int tile = blockIdx.x * blockDim.x; tile < L.nj; tile += gridDim.x * blockDim.x) {
-    const int j = tile + threadIdx.x;
-    const bool on = j < L.nj && L.task[j] >= 0;
+  const int lim = L.alist ? L.na : L.nj;
+  for (int tile = blockIdx.x * blockDim.x; tile < lim; tile += gridDim.x * blockDim.x) {
+    const int i = tile + threadIdx.x;
+    const int j = i < lim ? (L.alist ? L.alist[i] : i) : -1;
+    const int tk = j >= 0 ? L.task[j] : -1;
+    int beta = -1;
+    bool on = false;
+    if (tk >= 0) {
+      beta = L.comp[j];
+      if (beta == j) {
+        L.fp[j] = (unsigned)L.skey[tk];
+        L.lvl[j] = L.level;
+        L.task[j] = LV_DONE;
+      } else {
+        L.task[j] = beta;
+        on = true;
+      }
+    }
+    // class sizes: one atomic per class and warp, and the warps' first classes
+    // (a giant class fills whole tiles) merged once more across the block
+    const unsigned peers = __match_any_sync(0xffffffffu, beta);
+    const unsigned valid = __ballot_sync(0xffffffffu, beta >= 0);
+    const int first = valid ? __ffs(valid) - 1 : -1;
+    const bool infirst = first >= 0 && ((peers >> first) & 1u);
+    if (beta >= 0 && !infirst && lane == __ffs(peers) - 1) atomicAdd(L.csize + beta, __popc(peers));
+    if (lane == (first < 0 ? 0 : first)) {
+      wbeta[warp] = first < 0 ? -1 : beta;
+      wcnt[warp] = first < 0 ? 0 : __popc(peers);
+    }
     const unsigned m = __ballot_sync(0xffffffffu, on);
     if (lane == 0) wsum[warp] = __popc(m);
     __syncthreads();
+    if (warp == 0) {
+      const int b = lane < nw ? wbeta[lane] : -1;
+      const int c = lane < nw ? wcnt[lane] : 0;
+      const unsigned same = __match_any_sync(0xffffffffu, b);
+      const int tot = __reduce_add_sync(same, c);
+      if (b >= 0 && lane == __ffs(same) - 1) atomicAdd(L.csize + b, tot);
+    }
     if (threadIdx.x == 0) {
       int tot = 0;
       for (int w = 0; w < nw; w++) {
@@ -623,10 +658,9 @@ template <int K>
 __global__ void __launch_bounds__(256) k_lv_pins(LocArgs A, BigArgs Bg, LvArgs L, unsigned long long *J) {
   lv_pins<K>(A, Bg, L, J, LV_T0, LV_NT);
 }
-__global__ void __launch_bounds__(256) k_lv_jinit(LvArgs L, unsigned long long *J) { lv_jinit(L, J, LV_T0, LV_NT); }
-template <bool UP>
+template <bool UP, bool FIRST>
 __global__ void __launch_bounds__(256) k_lv_sweep(LvArgs L, const unsigned long long *Jc, unsigned long long *Jn) {
-  lv_sweep_round<UP>(L, Jc, Jn, L.ctr + LVC_CHANGED, LV_T0, LV_NT);
+  lv_sweep_round<UP, FIRST>(L, Jc, Jn, L.ctr + LVC_CHANGED, LV_T0, LV_NT);
 }
 __global__ void __launch_bounds__(256) k_lv_classes(LvArgs L) { lv_classes(L, L.ctr + LVC_ACTIVE, LV_T0, LV_NT); }
 __global__ void __launch_bounds__(256) k_lv_sortkeys(LvArgs L) { lv_sortkeys(L, LV_T0, LV_NT); }
@@ -719,24 +753,20 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
       for (int it = 0; it < 40; it++) {
         cslot = cslot == 2 ? 0 : cslot + 1;
         if (lead) ctr[LVK_CHANGED + (cslot == 2 ? 0 : cslot + 1)] = 0;
-        if (sweep == 0) lv_sweep_round<true>(L, Jc, Jn, ctr + LVK_CHANGED + cslot, t0, nt);
-        else lv_sweep_round<false>(L, Jc, Jn, ctr + LVK_CHANGED + cslot, t0, nt);
+        int *chg = ctr + LVK_CHANGED + cslot;
+        if (sweep == 0) lv_sweep_round<true, false>(L, Jc, Jn, chg, t0, nt);
+        else if (it == 0) lv_sweep_round<false, true>(L, Jc, Jn, chg, t0, nt);
+        else lv_sweep_round<false, false>(L, Jc, Jn, chg, t0, nt);
         grid.sync();
         unsigned long long *tmp = Jc;
         Jc = Jn;
         Jn = tmp;
-        if (*(volatile int *)(ctr + LVK_CHANGED + cslot) == 0) break;
-      }
-      if (sweep == 0) {
-        lv_jinit(L, Ja, t0, nt);
-        grid.sync();
+        if (*(volatile int *)chg == 0) break;
       }
     }
     LV_TICK(5)
-    lv_classes(L, nullptr, t0, nt);
-    grid.sync();
     int *lnext = bufs[apar];
-    lv_build_list(L, lnext, ctr + LVK_ACTIVE + apar);
+    lv_classes_list(L, lnext, ctr + LVK_ACTIVE + apar);
     grid.sync();
     LV_TICK(6)
     active = *(volatile int *)(ctr + LVK_ACTIVE + apar);

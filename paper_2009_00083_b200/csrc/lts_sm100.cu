@@ -698,16 +698,13 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
         for (int it = 0;; it++) {
           if (it >= 40) return lts_set_error(LTS_E_CUDA, "level flood: sweep did not converge");
           LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_CHANGED, 0, sizeof(int), s));
-          if (sweep == 0) k_lv_sweep<true><<<gj, 256, 0, s>>>(L, Jc, Jn);
-          else k_lv_sweep<false><<<gj, 256, 0, s>>>(L, Jc, Jn);
+          if (sweep == 0) k_lv_sweep<true, false><<<gj, 256, 0, s>>>(L, Jc, Jn);
+          else if (it == 0) k_lv_sweep<false, true><<<gj, 256, 0, s>>>(L, Jc, Jn);
+          else k_lv_sweep<false, false><<<gj, 256, 0, s>>>(L, Jc, Jn);
           g_launches++;
           std::swap(Jc, Jn);
           LTS_TRY(lv_read(c, LVC_CHANGED, 1));
           if (hc[LVC_CHANGED] == 0) break;
-        }
-        if (sweep == 0) {
-          k_lv_jinit<<<gj, 256, 0, s>>>(L, L.pm);
-          g_launches++;
         }
       }
       LTS_CUDA(cudaMemsetAsync(L.ctr + LVC_ACTIVE, 0, sizeof(int), s));
