@@ -409,7 +409,7 @@ def main():
     flood_bytes = (4.0 * K + 8.0) * flood_slots / max(flood_launches, 1)
     flood_gbs = flood_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0
     roofline = {"bound": "hbm", "kernel": "k_big_flood || k_lv_coop", "achieved": flood_gbs, "peak": hbm,
-                "unit": "GB/s", "frac": flood_gbs / hbm, "traffic": traffic.get("k_big_flood"),
+                "unit": "GB/s", "frac": flood_gbs / hbm, "traffic": traffic.get("k_big_flood || k_lv_coop", traffic.get("k_big_flood")),
                 "peak_source": peak_kind, "launches": flood_launches, "ms_per_launch": per_launch_ms,
                 "bytes_per_launch": flood_bytes,
                 "share_of_step": flood_ms / phases["total"] if phases["total"] else None,
