@@ -407,6 +407,10 @@ __device__ __forceinline__ void lv_jump(const LvArgs &L, int t0, int nt) {
 // max / min are idempotent, so the in-place updates of g need no ordering
 // beyond the barrier between rounds; the doubling tables are double-buffered.
 constexpr unsigned LV_NIL = 0xffffffffu;
+#ifndef LTS_LV_R4_MAX
+#define LTS_LV_R4_MAX (4 << 20)
+#endif
+constexpr int LV_R4_MAX = LTS_LV_R4_MAX;  // active vertices up to which a sweep round jumps four segments
 
 template <int K>
 __device__ __forceinline__ void lv_pins(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, unsigned long long *J,
@@ -442,9 +446,12 @@ __device__ __forceinline__ unsigned long long lv_j0(const LvArgs &L, int j, int 
 }
 
 // One doubling round.  FIRST: the pairs are read from the parent pointers (the
-// downward sweep restarts the doubling without an initialisation phase).  The
-// round reports whether any vertex still has an ancestor to jump to.
-template <bool UP, bool FIRST>
+// downward sweep restarts the doubling without an initialisation phase).  R4:
+// the round jumps four segments instead of two (it pushes to / pulls from the
+// ancestors at one, two and three segment lengths), halving the number of
+// rounds, i.e. grid barriers, of the small latency-bound floods.  The round
+// reports whether any vertex still has an ancestor to jump to.
+template <bool UP, bool FIRST, bool R4>
 __device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned long long *Jc, unsigned long long *Jn,
                                                int *changed, int t0, int nt) {
   int ch = 0;
@@ -453,22 +460,30 @@ __device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned l
     const int tk = L.task[j];
     if (tk < 0) continue;
     const unsigned long long a = FIRST ? lv_j0(L, j, tk) : Jc[j];
-    const unsigned anc = (unsigned)(a & 0xffffffffu);
+    unsigned anc = (unsigned)(a & 0xffffffffu);
     if (anc == LV_NIL) {
       Jn[j] = a;
       continue;
     }
-    const int pmin = (int)(a >> 32);  // smallest j in [j, anc)
-    if (UP) {
-      const int gv = g[j];
-      if (gv >= 0) atomicMax(g + anc, min(min(gv, pmin), (int)anc));
-    } else {
-      const int cand = min(pmin, g[anc]);
-      if (cand > g[j]) g[j] = cand;
+    int pmin = (int)(a >> 32);  // smallest j in [j, anc)
+    const int gv = UP ? g[j] : 0;
+    int hv = UP ? 0 : g[j];
+    const int hv0 = hv;
+#pragma unroll
+    for (int hop = 0; hop < (R4 ? 3 : 1); hop++) {
+      if (UP) {
+        if (gv >= 0) atomicMax(g + anc, min(min(gv, pmin), (int)anc));
+      } else {
+        hv = max(hv, min(pmin, g[anc]));
+      }
+      const unsigned long long b = FIRST ? lv_j0(L, (int)anc, tk) : Jc[anc];
+      pmin = min(pmin, (int)(b >> 32));
+      anc = (unsigned)(b & 0xffffffffu);
+      if (anc == LV_NIL) break;
     }
-    const unsigned long long b = FIRST ? lv_j0(L, (int)anc, tk) : Jc[anc];
-    Jn[j] = lv_pack((unsigned)min(pmin, (int)(b >> 32)), (unsigned)(b & 0xffffffffu));
-    if ((unsigned)(b & 0xffffffffu) != LV_NIL) ch = 1;
+    if (!UP && hv > hv0) g[j] = hv;
+    Jn[j] = lv_pack((unsigned)pmin, anc);
+    if (anc != LV_NIL) ch = 1;
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
@@ -660,7 +675,7 @@ __global__ void __launch_bounds__(256) k_lv_pins(LocArgs A, BigArgs Bg, LvArgs L
 }
 template <bool UP, bool FIRST>
 __global__ void __launch_bounds__(256) k_lv_sweep(LvArgs L, const unsigned long long *Jc, unsigned long long *Jn) {
-  lv_sweep_round<UP, FIRST>(L, Jc, Jn, L.ctr + LVC_CHANGED, LV_T0, LV_NT);
+  lv_sweep_round<UP, FIRST, false>(L, Jc, Jn, L.ctr + LVC_CHANGED, LV_T0, LV_NT);
 }
 __global__ void __launch_bounds__(256) k_lv_classes(LvArgs L) { lv_classes(L, L.ctr + LVC_ACTIVE, LV_T0, LV_NT); }
 __global__ void __launch_bounds__(256) k_lv_sortkeys(LvArgs L) { lv_sortkeys(L, LV_T0, LV_NT); }
@@ -754,9 +769,16 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
         cslot = cslot == 2 ? 0 : cslot + 1;
         if (lead) ctr[LVK_CHANGED + (cslot == 2 ? 0 : cslot + 1)] = 0;
         int *chg = ctr + LVK_CHANGED + cslot;
-        if (sweep == 0) lv_sweep_round<true, false>(L, Jc, Jn, chg, t0, nt);
-        else if (it == 0) lv_sweep_round<false, true>(L, Jc, Jn, chg, t0, nt);
-        else lv_sweep_round<false, false>(L, Jc, Jn, chg, t0, nt);
+        // few active vertices: the barriers dominate, jump four segments a round
+        if (L.na <= LV_R4_MAX) {
+          if (sweep == 0) lv_sweep_round<true, false, true>(L, Jc, Jn, chg, t0, nt);
+          else if (it == 0) lv_sweep_round<false, true, true>(L, Jc, Jn, chg, t0, nt);
+          else lv_sweep_round<false, false, true>(L, Jc, Jn, chg, t0, nt);
+        } else {
+          if (sweep == 0) lv_sweep_round<true, false, false>(L, Jc, Jn, chg, t0, nt);
+          else if (it == 0) lv_sweep_round<false, true, false>(L, Jc, Jn, chg, t0, nt);
+          else lv_sweep_round<false, false, false>(L, Jc, Jn, chg, t0, nt);
+        }
         grid.sync();
         unsigned long long *tmp = Jc;
         Jc = Jn;
