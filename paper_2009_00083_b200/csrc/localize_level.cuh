@@ -45,7 +45,8 @@ namespace cg = cooperative_groups;
 
 constexpr int LV_DONE = -1;
 constexpr unsigned LV_NONE = 0xffffffffu;
-enum { LVC_HOOKS = 0, LVC_CHANGED = 1, LVC_ACTIVE = 2, LVC_ERR = 3, LVC_N = 12 };
+constexpr int LV_INTERIOR = -(1 << 30);  // lvl mark during the forest rounds
+enum { LVC_HOOKS = 0, LVC_CHANGED = 1, LVC_ACTIVE = 2, LVC_N = 16 };
 
 struct LvArgs {
   int *task;    // j: source (j index) of the flood task the vertex belongs to, LV_DONE when placed
@@ -314,6 +315,9 @@ __device__ __forceinline__ void lv_scan(const LocArgs &A, const BigArgs &Bg, con
     if (tk < 0) continue;
     const int c = L.comp[j];
     if (c == tk) continue;
+    // a vertex whose neighbours all share its component stays interior for the
+    // rest of the forest (components only merge): skipped from then on
+    if (L.lvl[j] == LV_INTERIOR) continue;
     const LvRef R = lv_ref(A, Bg, j);
     int q[K];
     lv_load_row<K>(Bg, R, j, q);
@@ -335,6 +339,7 @@ __device__ __forceinline__ void lv_scan(const LocArgs &A, const BigArgs &Bg, con
       b = max(b, w);
     }
     if (b) atomicMax(L.best + c, b);
+    else L.lvl[j] = LV_INTERIOR;
   }
 }
 
@@ -691,7 +696,8 @@ __global__ void __launch_bounds__(256) k_lv_write(LocArgs A, BigArgs Bg, LvArgs 
 // the hook counter alternates between two slots (read before the round's last
 // barrier), the changed flag rotates over three (read after its barrier), the
 // active count alternates by level.
-enum { LVK_HOOKS = 0, LVK_CHANGED = 2, LVK_ACTIVE = 5, LVK_INIT = 7, LVK_LEVELS = 8, LVK_ROUNDS = 9, LVK_NSRC = 10 };
+enum { LVK_HOOKS = 0, LVK_CHANGED = 2, LVK_ACTIVE = 5, LVK_INIT = 7, LVK_LEVELS = 8, LVK_ROUNDS = 9, LVK_NSRC = 10,
+       LVK_ERR = 12 };  // LVK_ERR: a loop hit its round limit (the host turns it into an error)
 
 // phase clocks of the lead thread (LTS_LEVEL_VERBOSE): chain, prep, scan, hook, jump, beta, classes
 __device__ long long d_lvclk[8];
@@ -736,6 +742,7 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
       grid.sync();
       LV_TICK(4)
       if (h == 0) break;
+      if (round == 63 && lead) ctr[LVK_ERR] = 1;
     }
   }
   L.level = 0;
@@ -784,6 +791,7 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
         Jc = Jn;
         Jn = tmp;
         if (*(volatile int *)chg == 0) break;
+        if (it == 39 && lead) ctr[LVK_ERR] = 1;
       }
     }
     LV_TICK(5)
@@ -815,6 +823,7 @@ __global__ void __launch_bounds__(512) k_lv_pos_coop(LvArgs L) {
     lv_pos_round(L, L.ctr + LVK_CHANGED + cslot, t0, nt);
     grid.sync();
     if (*(volatile int *)(L.ctr + LVK_CHANGED + cslot) == 0) break;
+    if (it == 63 && t0 == 0) L.ctr[LVK_ERR] = 1;
   }
 }
 

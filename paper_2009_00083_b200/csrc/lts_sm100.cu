@@ -256,8 +256,8 @@ enum {
   SC_BIGWORK = 34,  // 2 ints: 64-bit sum of region sizes flooded by k_big_flood
   SC_BIGSLOTS = 36, // = SC_NBIG + 7: slots of the big regions
   SC_BVSTATE = 40,  // 2: active roots of the last Boruvka round, rounds run
-  SC_LV = 44,       // LVC_N (12) counters of the level-parallel floods
-  SC_LVTMP = 56,
+  SC_LV = 44,       // LVC_N (16) counters of the level-parallel floods
+  SC_LVTMP = 60,
   SC_N = 64
 };
 
@@ -1020,7 +1020,11 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       // launch is already queued on the main stream
       for (;;) {
         LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_BIGACT, w.scal + SC_BIGACT, 4 * sizeof(int), cudaMemcpyDeviceToHost, g_bigs));
+        LTS_CUDA(cudaMemcpyAsync(c.h_scal + SC_LV + LVK_ERR, w.scal + SC_LV + LVK_ERR, sizeof(int), cudaMemcpyDeviceToHost,
+                                 g_bigs));
         LTS_CUDA(cudaStreamSynchronize(g_bigs));
+        if (g_nlevel > 0 && c.h_scal[SC_LV + LVK_ERR])
+          return lts_set_error(LTS_E_CUDA, "level flood: a loop hit its round limit");
         if (c.h_scal[SC_BIGACT] == 0) {
           c.flood_slots += *reinterpret_cast<const long long *>(c.h_scal + SC_BIGWORK);
           break;
