@@ -719,13 +719,15 @@ __global__ void k_region_slots(const int *__restrict__ rsize, int R, int *tmp) {
 }
 
 __global__ void k_place(const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sval, int C,
-                        const int *__restrict__ rptr, int *verts, int *loc_of) {
+                        const int *__restrict__ rptr, int *verts, int *slot_of) {
+  // slot_of is the region-label array: claimed vertices trade their region id
+  // for their slot (>= 1), unclaimed ones keep -1
   GRID_STRIDE(j, C) {
     int rid = (int)skey[j];
     int v = (int)sval[j];
     int slot = (int)j + rid + 1;
     verts[slot] = v;
-    loc_of[v] = slot - rptr[rid];
+    slot_of[v] = slot;
   }
 }
 

@@ -30,8 +30,7 @@ struct LocArgs {
   int R;
   const int *rptr;    // R+1 slot offsets
   const int *verts;   // slots: vertex ids, saddle first
-  const int *reg_of;  // vertex -> region id or -1
-  const int *loc_of;  // vertex -> local index
+  const int *slot_of;  // vertex -> its slot in `verts` (claimed vertices), -1 otherwise
   int *buf0, *buf1, *buf2;  // slot arrays: rotating flood states
   int *out;                 // slot array: final local order
   unsigned long long *gheap;  // slot array: global heap scratch
@@ -85,11 +84,13 @@ __device__ __forceinline__ unsigned long long hkey(int key, int p) {
   return ((unsigned long long)(unsigned)key << 32) | (unsigned)p;
 }
 
-// local index of vertex u within region rid (saddle s at index 0), or -1
-__device__ __forceinline__ int member(const LocArgs &A, int u, int rid, int s) {
+// local index of vertex u within the region of slots [lo, lo + k) (saddle s at
+// index 0), or -1: one read of the vertex's global slot (k_place)
+__device__ __forceinline__ int member(const LocArgs &A, int u, int lo, int k, int s) {
   if (u < 0) return -1;
   if (u == s) return 0;
-  return A.reg_of[u] == rid ? A.loc_of[u] : -1;
+  const int d = A.slot_of[u] - lo;
+  return d > 0 && d < k ? d : -1;
 }
 
 // One exact priority flood.  desc: source = saddle, max-key first, label
@@ -141,7 +142,7 @@ __device__ void flood(const LocArgs &A, bool asc, int rid, int s, int k, const i
     if (lane < K) {
       const Nb<NDIM> nb(A.g, v);
       int u = nb(A.g, lane);
-      q = member(A, u, rid, s);
+      q = member(A, u, (int)(verts - A.verts), k, s);
       if (q >= 0) {
         if (sfl[q] & SF_INHEAP) {
           q = -1;
@@ -179,7 +180,7 @@ __device__ bool check_minima(const LocArgs &A, int rid, int s, int k, const int 
     bool mn = true;
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
-      int q = member(A, nb(A.g, kk), rid, s);
+      int q = member(A, nb(A.g, kk), (int)(verts - A.verts), k, s);
       if (q >= 0 && cur[q] < c) {
         mn = false;
         break;
@@ -208,7 +209,7 @@ __device__ bool check_maxima(const LocArgs &A, int rid, int s, int k, const int 
     bool mx = true;
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
-      int q = member(A, nb(A.g, kk), rid, s);
+      int q = member(A, nb(A.g, kk), (int)(verts - A.verts), k, s);
       if (q >= 0 && cur[q] > c) {
         mx = false;
         break;

@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(256) k_big_rows(LocArgs A, BigArgs Bg) {
 #pragma unroll
       for (int kk = 0; kk < K; kk++) {
         int u = nb(A.g, kk);
-        const int q = member(A, u, rid, s);
+        const int q = member(A, u, lo, A.rptr[rid + 1] - lo, s);
         row[kk] = q;
         if (q > p) top = false;
         if (p >= 1 && u >= 0 && eff_rank(A.rank, u, A.rev, n) < srank) out = true;

@@ -913,7 +913,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     C = c.h_scal[SC_C];
     LTS_CUDA(cudaMemcpyAsync(w.rptr + R, w.scal + SC_S, sizeof(int), cudaMemcpyDeviceToDevice, s));
     LTS_TRY(radix_sort(w.ckey, w.cval, C, bits_for(R - 1), false, w.skey, w.sval, nullptr, w.sb, s));
-    k_place<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, w.loc_of);
+    k_place<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, w.reg_of);
     k_place_saddles<<<NB(R), 256, 0, s>>>(inv, rev, ni, w.rsad, R, w.rptr, w.verts);
     // schedule: largest region first (stable by region id)
     k_order_keys<<<NB(R), 256, 0, s>>>(w.rsize, R, (uint32_t *)w.okey);
@@ -925,7 +925,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     Phase ph(c, LTS_PH_LOCALIZE);
     LocArgs A;
     A.g = c.g; A.rank = rank; A.rev = rev; A.order = w.order; A.R = R; A.rptr = w.rptr;
-    A.verts = w.verts; A.reg_of = w.reg_of; A.loc_of = w.loc_of; A.buf0 = w.buf0; A.buf1 = w.buf1;
+    A.verts = w.verts; A.slot_of = w.reg_of; A.buf0 = w.buf0; A.buf1 = w.buf1;
     A.buf2 = w.buf2; A.out = w.out; A.gheap = w.gheap; A.sfl = w.sfl; A.n_iters = w.nit;
     A.status = w.st; A.max_iter = max_iter; A.queue = w.scal + SC_QUEUE; A.qbase = 0;
     const int nbig = c.h_scal[SC_NBIG];
