@@ -161,10 +161,10 @@ __global__ void k_hash_compact(EdgeHash H, int *ea, int *eb, int *ew, int *cnt) 
   }
 }
 
-// Cross-manifold edges of the maxima graph.  Every grid edge is owned by its
-// lower endpoint u (weight = rank u), and u emits one edge per DISTINCT
-// neighbouring manifold: all of u's edges into the same manifold carry the
-// same weight, so the duplicates cannot change any bottleneck.  A CTA owns a
+// Cross-manifold edges of the maxima graph.  Every grid edge is visited once,
+// from its endpoint with the forward stencil offset, with the weight of its
+// lower endpoint's rank; a vertex emits one edge per DISTINCT neighbouring
+// manifold (its heaviest), so duplicates cannot change any bottleneck.  A CTA owns a
 // 32 x 16 (x, y) column of the grid and marches in z (8-plane chunks) (one z plane for 2D grids); the manifold labels M and the
 // ranks of planes z-1..z+1 sit in a 5-slot shared-memory ring with halo, so
 // the 14-neighbour tests never touch L1/L2.  Edges found by the CTA are
@@ -322,24 +322,30 @@ __global__ void __launch_bounds__(ET_NT) k_edges_tile(Grid g, const int *__restr
     const int *m0 = sM[NDIM == 2 ? 0 : s1], *mm = sM[NDIM == 2 ? 0 : sm], *mp = sM[NDIM == 2 ? 0 : s2];
     const int *r0 = sR[NDIM == 2 ? 0 : s1], *rm_ = sR[NDIM == 2 ? 0 : sm], *rp = sR[NDIM == 2 ? 0 : s2];
     int a = -1, rv = -1;
-    int d0 = -1, d1 = -1, d2 = -1;  // distinct higher neighbour manifolds (first three)
+    // Every grid edge is visited once, from its endpoint with the forward
+    // stencil offset (the first K/2 offsets): weight = the lower endpoint's
+    // rank.  Up to three distinct neighbouring manifolds are kept per vertex
+    // with their heaviest edge; further ones go straight to the shared table.
+    int d0 = -1, d1 = -1, d2 = -1, w0 = -1, w1 = -1, w2 = -1;
     if (x < nx && y < ny) {
       a = m0[c];
       rv = r0[c];
 #pragma unroll
-      for (int k = 0; k < K; k++) {
+      for (int k = 0; k < K / 2; k++) {
         const int dz = St::dz(k);
         const int o = c + St::dx(k) + ET_PX * St::dy(k);
-        const int *mk = dz == 0 ? m0 : (dz > 0 ? mp : mm);
-        const int *rk = dz == 0 ? r0 : (dz > 0 ? rp : rm_);
+        const int *mk = dz == 0 ? m0 : mp;
+        const int *rk = dz == 0 ? r0 : rp;
         const int b = mk[o];
         if (b == a || b < 0) continue;
-        if (rk[o] < rv) continue;                      // owned by the lower endpoint
-        if (b == d0 || b == d1 || b == d2) continue;  // same weight rv: a duplicate
-        if (d0 < 0) d0 = b;
-        else if (d1 < 0) d1 = b;
-        else if (d2 < 0) d2 = b;
-        else et_insert(hkey, hw, &hcount, H, vcls, bestP, ea, eb, ew, ecount, a, b, rv);  // rare
+        const int w = min(rv, rk[o]);
+        if (b == d0) w0 = max(w0, w);
+        else if (b == d1) w1 = max(w1, w);
+        else if (b == d2) w2 = max(w2, w);
+        else if (d0 < 0) { d0 = b; w0 = w; }
+        else if (d1 < 0) { d1 = b; w1 = w; }
+        else if (d2 < 0) { d2 = b; w2 = w; }
+        else et_insert(hkey, hw, &hcount, H, vcls, bestP, ea, eb, ew, ecount, a, b, w);  // rare
       }
     }
     // warp aggregation (32 consecutive x voxels usually border the same
@@ -347,13 +353,16 @@ __global__ void __launch_bounds__(ET_NT) k_edges_tile(Grid g, const int *__restr
 #pragma unroll
     for (int i = 0; i < 3; i++) {
       const int b = i == 0 ? d0 : (i == 1 ? d1 : d2);
+      const int w = i == 0 ? w0 : (i == 1 ? w1 : w2);
       const bool has = b >= 0;
       if (!__any_sync(0xffffffffu, has)) break;
       const unsigned lo = (unsigned)min(a, b), hi = (unsigned)max(a, b);
       const unsigned long long key = has ? (((unsigned long long)lo << 32) | hi) : ~0ull;
       const unsigned peers = __match_any_sync(0xffffffffu, key);
-      const int best = __reduce_max_sync(peers, rv);
-      if (has && rv == best) et_insert(hkey, hw, &hcount, H, vcls, bestP, ea, eb, ew, ecount, a, b, rv);
+      const int best = __reduce_max_sync(peers, w);
+      const unsigned top = __ballot_sync(0xffffffffu, has && w == best) & peers;
+      if (has && (threadIdx.x & 31) == __ffs(top) - 1)
+        et_insert(hkey, hw, &hcount, H, vcls, bestP, ea, eb, ew, ecount, a, b, w);
     }
     sm = s1;
   }

@@ -655,7 +655,15 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
     }
     // one block per SM keeps the grid barriers short; large key spaces take
     // more blocks for memory parallelism
-    lv_grid = d.lv_blocks[nd] * std::min(d.lv_per[nd], L.nj >= (1 << 20) ? 2 : 1);
+    {
+      static int per_env = -1;  // LTS_LV_PER: CTAs per SM of the cooperative grid (tuning)
+      if (per_env < 0) {
+        const char *e = getenv("LTS_LV_PER");
+        per_env = e ? atoi(e) : 0;
+      }
+      const int want = per_env > 0 ? per_env : (L.nj >= (1 << 20) ? 2 : 1);
+      lv_grid = d.lv_blocks[nd] * std::min(d.lv_per[nd], want);
+    }
     lv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(lv_grid, ((int64_t)L.nj + 511) / 512));
     void *kargs[] = {(void *)&A, (void *)&B, (void *)&L};
     LTS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(lv_grid), dim3(512), kargs, 0, s));
