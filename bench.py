@@ -236,6 +236,7 @@ def other_configs(dev, budget_s: float):
             "oracle_cpu_s": (d.get("oracle_seconds") or {}).get("simplify"),
         }
         del fd, F, g, G
+        N.release_workspaces()  # the next config allocates its own workspace into free memory
         torch.cuda.empty_cache()
     return out
 

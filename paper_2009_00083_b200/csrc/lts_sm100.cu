@@ -152,7 +152,7 @@ struct DevState {
   cudaStream_t side = nullptr, side2 = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, lfork = nullptr, ljoin = nullptr;
   bool big_attr = false;
-  int coop_blocks = 0;
+  int coop_blocks = 0, coop_per = 0;  // SMs and resident CTAs per SM of k_bv_coop
   int lv_blocks[4] = {0, 0, 0, 0}, lv_per[4] = {0, 0, 0, 0};  // cooperative grid of the level floods, per ndim
 };
 static DevState g_dev[LTS_MAX_DEV];
@@ -863,14 +863,17 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     // Boruvka rounds: tau(m) = bottleneck to preserved maxima, all rounds in
     // one cooperative launch (grid barriers between phases); one readback
     {
-      int &coop_blocks = g_cur->coop_blocks;
-      if (!coop_blocks) {
-        int dev = 0, nsm = 0, per = 0;
+      // one CTA per SM keeps the grid barriers short; graphs with many maxima
+      // (hundreds of edges per thread and round) take four
+      int &coop_sm = g_cur->coop_blocks, &coop_per = g_cur->coop_per;
+      if (!coop_sm) {
+        int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bv_coop, 256, 0);
-        coop_blocks = std::max(1, std::min(per, LTS_BV_COOP_PER_SM)) * nsm;
+        cudaDeviceGetAttribute(&coop_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&coop_per, k_bv_coop, 256, 0);
+        coop_per = std::max(1, coop_per);
       }
+      const int coop_blocks = coop_sm * std::min(coop_per, nm >= (1 << 18) ? 4 : LTS_BV_COOP_PER_SM);
       BvArgs ba{w.mlist, nm, w.comp, w.par, w.wc, w.rt, w.acc, w.scal + SC_ERR, w.cst, w.vcls, w.bestP, w.best,
                 ea, eb, ew, w.scal + SC_ECOUNT, w.scal + SC_BVSTATE};
       void *kargs[] = {&ba};
@@ -987,6 +990,14 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       LTS_CUDA(cudaStreamSynchronize(g_bigs));
       g_nlevel = c.h_scal[SC_BIGACT + 1];
       LTS_TRY(big_iteration(c, A, B, big_gx));
+      // A cooperative flood over millions of keys pays for every grid barrier
+      // with the slowest CTA: sharing the SMs with the warp floods below slows
+      // it by far more than those take (cfg5: 600 vs 370 ms), so the main
+      // stream waits for the first flood of large key spaces.
+      if (g_nlevel > 0 && g_bigs != s && B.bslots >= (4 << 20)) {
+        LTS_CUDA(cudaEventRecord(g_cur->join, g_bigs));
+        LTS_CUDA(cudaStreamWaitEvent(s, g_cur->join, 0));
+      }
     }
     A.qbase = nbig;
     if (R > nbig) {

@@ -61,6 +61,10 @@ def run(cfg, repeat):
            "G_match": sha(G.cpu().numpy()) == ref.get("G_sha"),
            "g_match": sha(g.cpu().numpy()) == ref.get("g_sha"), "gen_s": round(tgen, 1)}
     print(json.dumps(out), flush=True)
+    # free this config's buffers and workspace before the next config allocates its own
+    del fd, F, g, G, pm_d, pn_d
+    P._native.release_workspaces()
+    torch.cuda.empty_cache()
     return out
 
 
