@@ -46,6 +46,7 @@ namespace cg = cooperative_groups;
 constexpr int LV_DONE = -1;
 constexpr unsigned LV_NONE = 0xffffffffu;
 constexpr int LV_INTERIOR = -(1 << 30);  // lvl mark during the forest rounds
+constexpr int LV_CHAIN = 1 << 29;        // lvl of a prefix vertex: LV_CHAIN | its place after the source
 enum { LVC_HOOKS = 0, LVC_CHANGED = 1, LVC_ACTIVE = 2, LVC_N = 16 };
 
 struct LvArgs {
@@ -272,9 +273,11 @@ __device__ __forceinline__ void lv_prefix(const LocArgs &A, const BigArgs &Bg, c
       bi = __shfl_sync(0xffffffffu, bi, __ffs(own) - 1);
       if (lane == 0) {
         fr[bi] = fr[nf - 1];
+        // the i-th prefix vertex sits i places after the source: it hangs off p
+        // directly with that offset, so the prefix adds no depth to F
         L.task[z] = LV_DONE;
-        L.fp[z] = (unsigned)prev;
-        L.lvl[z] = L.level;
+        L.fp[z] = (unsigned)p;
+        L.lvl[z] = LV_CHAIN | (steps + 1);
         L.csize[z] = 1;
         L.sval[z] = p;
       }
@@ -619,7 +622,9 @@ __device__ __forceinline__ void lv_off(const LocArgs &A, const BigArgs &Bg, cons
     const unsigned f = L.fp[j];
     if (f == LV_NONE) continue;
     int acc = L.sval[i] - L.par[f] + 1;
-    if (L.fp[f] == LV_NONE && lv_ref(A, Bg, j).asc) acc--;  // children of the virtual root start at 0
+    const int lv = L.lvl[j];
+    if (lv >= LV_CHAIN) acc = lv - LV_CHAIN;  // prefix vertex: its place after the source
+    else if (L.fp[f] == LV_NONE && lv_ref(A, Bg, j).asc) acc--;  // children of the virtual root start at 0
     L.pm[j] = lv_pack((unsigned)acc, f);
   }
 }

@@ -994,7 +994,12 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
       // with the slowest CTA: sharing the SMs with the warp floods below slows
       // it by far more than those take (cfg5: 600 vs 370 ms), so the main
       // stream waits for the first flood of large key spaces.
-      if (g_nlevel > 0 && g_bigs != s && B.bslots >= (4 << 20)) {
+      static int solo = -1;  // LTS_LEVEL_SOLO: key-space size from which the main stream waits
+      if (solo < 0) {
+        const char *e = getenv("LTS_LEVEL_SOLO");
+        solo = e ? atoi(e) : (4 << 20);
+      }
+      if (g_nlevel > 0 && g_bigs != s && B.bslots >= solo) {
         LTS_CUDA(cudaEventRecord(g_cur->join, g_bigs));
         LTS_CUDA(cudaStreamWaitEvent(s, g_cur->join, 0));
       }
