@@ -310,7 +310,7 @@ __device__ __forceinline__ void lv_prep(const LvArgs &L, int t0, int nt) {
 
 // Boruvka round, step 1: every vertex outside its task's root component offers
 // its heaviest edge leaving its component (weight: (min j, max j), the root
-// and its contracted chain counting as +infinity) to the component's label
+// counting as +infinity) to the component's label
 template <int K>
 __device__ __forceinline__ void lv_scan(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, int t0, int nt) {
   LV_FOR(j, L) {
@@ -328,16 +328,15 @@ __device__ __forceinline__ void lv_scan(const LocArgs &A, const BigArgs &Bg, con
 #pragma unroll
     for (int kk = 0; kk < K; kk++) {
       if (q[kk] < 0) continue;
+      // the forest is built on the level-1 graph: every neighbour row entry is a
+      // member of the same task, or the region's source itself
       const int u = R.jb + q[kk];
-      const int tu = L.task[u];
       unsigned long long w;
-      if (tu == tk) {
-        if (L.comp[u] == c) continue;
-        w = lv_pack((unsigned)min(u, j), (unsigned)max(u, j));
-      } else if (tu < 0 && (u == tk || L.sval[u] == tk)) {
+      if (u == tk) {
         w = lv_pack((unsigned)j, LV_NONE);
       } else {
-        continue;
+        if (L.comp[u] == c) continue;
+        w = lv_pack((unsigned)min(u, j), (unsigned)max(u, j));
       }
       b = max(b, w);
     }
