@@ -213,11 +213,19 @@ __device__ __forceinline__ void lv_chain(const LocArgs &A, const BigArgs &Bg, co
 // from the source plus that prefix.  One warp per task source runs the plain
 // priority flood with its frontier in shared memory: as long as it climbs
 // (every step of an ascent is free: the chain rule above), and otherwise for a
-// budget of steps proportional to the task's size, so that the sequential
-// prefix costs about as much as the level's sweeps over the task.  On a climb
+// budget of steps proportional to the task's size (at least 32 for tasks of
+// 1 K vertices: about the latency of a level's barriers), so that the
+// sequential prefix costs about as much as the level's sweeps over the task.  On a climb
 // through a bumpy field a level then crosses many bumps instead of one.
 constexpr int LV_FCAP = 704;    // frontier entries per warp (static shared memory: 16 x 704 ints)
 constexpr int LV_WARPS = 16;    // warps per block of the cooperative kernel
+#ifndef LTS_LV_MINB
+#define LTS_LV_MINB 32
+#endif
+#ifndef LTS_LV_MINB_SIZE
+#define LTS_LV_MINB_SIZE 1024
+#endif
+constexpr int LV_MINB = LTS_LV_MINB, LV_MINB_SIZE = LTS_LV_MINB_SIZE;  // least prefix budget of tasks of that size
 
 __device__ __forceinline__ void lv_sources(const LvArgs &L, const int *plist, int np, int *srclist, int *nsrc,
                                            int t0, int nt) {
@@ -238,7 +246,7 @@ __device__ __forceinline__ void lv_prefix(const LocArgs &A, const BigArgs &Bg, c
   for (int si = t0 >> 5; si < ns; si += nt >> 5) {
     const int p = srclist[si];
     const LvRef R = lv_ref(A, Bg, p);
-    const int budget = min(4096, L.csize[p] >> 13);
+    const int budget = min(4096, max(L.csize[p] >> 13, L.csize[p] >= LV_MINB_SIZE ? LV_MINB : 0));
     int nf = 0, cur = p, last = -1, prev = p, steps = 0;
     for (;;) {
       // the unplaced member neighbours of the vertex just placed join the frontier
