@@ -309,12 +309,24 @@ static int64_t carve(WS *w, char *base, int ndim, int64_t n) {
   w->sb.nonfinite = i32(4);
   w->bsum = i32(n / SCAN_TILE + 2);
   {
-    // key space of the large regions: one entry per slot plus one per region
+    // key space of the large regions: one entry per slot plus one per region.
+    // The maxima-graph edge buffer is idle between discover and the next pass:
+    // the level arrays live in it as far as they fit.
     const int64_t nj = s2 + n1 / BIG_THRESHOLD + 8;
-    w->lv.task = i32(nj); w->lv.fp = u32(nj); w->lv.par = i32(nj); w->lv.comp = i32(nj); w->lv.link = i32(nj);
-    w->lv.csize = i32(nj); w->lv.lvl = i32(nj); w->lv.skey = i32(nj); w->lv.sval = i32(nj); w->lv.oval = i32(nj);
-    w->lv.best = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)nj);
-    w->lv.pm = (unsigned long long *)take(sizeof(unsigned long long) * (size_t)nj);
+    size_t eoff = 0;
+    const size_t ecap = 12 * (size_t)w->emax;
+    auto etake = [&](size_t bytes) -> char * {
+      const size_t at = (eoff + 255) & ~(size_t)255;
+      if (at + bytes > ecap) return take(bytes);
+      eoff = at + bytes;
+      return base ? w->ebuf + at : nullptr;
+    };
+    auto ei32 = [&](int64_t cnt) { return (int *)etake(sizeof(int) * (size_t)cnt); };
+    w->lv.best = (unsigned long long *)etake(sizeof(unsigned long long) * (size_t)nj);
+    w->lv.pm = (unsigned long long *)etake(sizeof(unsigned long long) * (size_t)nj);
+    w->lv.task = ei32(nj); w->lv.fp = (unsigned *)ei32(nj); w->lv.par = ei32(nj); w->lv.comp = ei32(nj);
+    w->lv.link = ei32(nj); w->lv.csize = ei32(nj); w->lv.lvl = ei32(nj); w->lv.skey = ei32(nj);
+    w->lv.sval = ei32(nj); w->lv.oval = ei32(nj);
     // the final sort runs after the levels: its ping-pong buffers reuse the Boruvka arrays
     w->lsb.k1 = (uint32_t *)w->lv.comp; w->lsb.v1 = (uint32_t *)w->lv.link;
     w->lsb.k2 = (uint32_t *)w->lv.best; w->lsb.v2 = w->lsb.k2 ? w->lsb.k2 + nj : nullptr;
