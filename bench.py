@@ -424,17 +424,17 @@ def main():
     G_host = torch.empty(n, dtype=torch.int32).pin_memory()
     pm_h = torch.from_numpy(pm).pin_memory()
     pn_h = torch.from_numpy(pn).pin_memory()
-    f_in = torch.empty(n, dtype=torch.float32, device=dev)
-    pm_in = torch.empty_like(pm_d)
-    pn_in = torch.empty_like(pn_d)
+    # the public host-buffer call (engine.simplify_field_host -> lts_simplify_host):
+    # pinned f and preserve lists in, pinned g and G out, every copy inside
+    pres_h = P.ConstraintSet(preserveMinima=pn_h.numpy(), preserveMaxima=pm_h.numpy())
+    with torch.cuda.device(dev):
+        gq, Gq, _ = P.simplify_field_host(mesh, f_host, pres_h, opt, g_host, G_host, device=dev)
+    torch.cuda.synchronize()
+    # the host outputs equal the device-resident call's
+    assert torch.equal(G_host, G.cpu()) and g_host.numpy().tobytes() == g.cpu().numpy().tobytes()
 
     def e2e_step():
-        f_in.copy_(f_host, non_blocking=True)
-        pm_in.copy_(pm_h, non_blocking=True)
-        pn_in.copy_(pn_h, non_blocking=True)
-        gg, GG, _ = P.simplify_raw(mesh, f_in, pm_in, pn_in, None, opt, g, G)
-        g_host.copy_(gg, non_blocking=True)
-        G_host.copy_(GG, non_blocking=True)
+        P.simplify_field_host(mesh, f_host, pres_h, opt, g_host, G_host, device=dev)
 
     e2e_step()
     torch.cuda.synchronize()

@@ -212,6 +212,19 @@ int lts_remove_pass_csr(int kind, const int32_t *rank, const int32_t *inverse, c
                         int32_t *new_inverse, float *g, lts_pass_report_t *rep, lts_regions_view_t *view, void *ws,
                         size_t ws_bytes, void *stream);
 
+/* lts_simplify with HOST buffers, the form the reference's numpy-facing
+ * simplify_field binds directly: f_host (float32 n), the
+ * preserve lists (int64) and the outputs g_host (float32 n) / G_host (int32 n)
+ * are host memory (page-locked for asynchronous copies).  dev: device scratch
+ * of lts_host_scratch_size bytes (f, g and the lists on the device).  The
+ * copy of g to the host is queued as soon as the last pass has realised it,
+ * beside that pass's floods; the call returns with both outputs complete. */
+int lts_host_scratch_size(int ndim, const int64_t *dims, int64_t n_max, int64_t n_min, size_t *bytes);
+int lts_simplify_host(const float *f_host, int ndim, const int64_t *dims, const int64_t *pres_max_host,
+                      int64_t n_max, const int64_t *pres_min_host, int64_t n_min, float *g_host,
+                      int32_t *G_host, lts_report_t *rep, const lts_options_t *opt, void *dev,
+                      size_t dev_bytes, void *ws, size_t ws_bytes, void *stream);
+
 /* lts_simplify on an explicit mesh (SPEC.md:348-356 over any triangulation). */
 int lts_simplify_csr(const float *f, int64_t n, const int32_t *indptr, const int32_t *indices,
                      const int64_t *pres_max, int64_t n_max, const int64_t *pres_min, int64_t n_min,

@@ -15,7 +15,8 @@ from .order import (OrderField, ScalarField, ZetaMode, ZetaPolicy, compute_order
 from .critical import (CriticalSet, Criticality, Kind, classify_all, classify_vertex,
                        extract_critical_points, extrema)
 from .engine import (ConstraintSet, PassRegions, SimplifyOptions, SimplifyReport, discover_regions,
-                     remove_extrema, remove_pass, simplify_field, simplify_raw, verify_constraints)
+                     remove_extrema, remove_pass, simplify_field, simplify_field_host, simplify_raw,
+                     verify_constraints)
 from .persistence import (PersistencePairs, compute_extremum_saddle_pairs, persistence_curve,
                           persistence_simplify)
 
@@ -26,7 +27,7 @@ __all__ = [
     "load_off", "write_off", "make_octahedron", "make_icosahedron", "make_torus", "OrderField", "ScalarField", "ZetaMode", "ZetaPolicy", "compute_order_field",
     "order_from_ranks", "realize_numeric", "CriticalSet", "Criticality", "Kind", "classify_all", "classify_vertex",
     "extract_critical_points", "extrema", "ConstraintSet", "PassRegions", "SimplifyOptions",
-    "SimplifyReport", "discover_regions", "remove_extrema", "remove_pass", "simplify_field",
+    "SimplifyReport", "discover_regions", "remove_extrema", "remove_pass", "simplify_field", "simplify_field_host",
     "simplify_raw", "verify_constraints", "PersistencePairs", "compute_extremum_saddle_pairs",
     "persistence_curve", "persistence_simplify",
 ]

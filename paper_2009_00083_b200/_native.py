@@ -67,7 +67,8 @@ class lts_regions_view_t(ctypes.Structure):
 EXPORTS = ["lts_version", "lts_last_error", "lts_workspace_size", "lts_order_field", "lts_classify",
            "lts_remove_pass", "lts_simplify", "lts_kernel_launches", "lts_debug_big_stats", "lts_bench_kernels",
            "lts_extremum_pairs", "lts_check_field", "lts_realize_numeric", "lts_workspace_size_csr",
-           "lts_classify_csr", "lts_remove_pass_csr", "lts_simplify_csr"]
+           "lts_classify_csr", "lts_remove_pass_csr", "lts_simplify_csr", "lts_host_scratch_size",
+           "lts_simplify_host"]
 
 _lib = None
 
@@ -107,6 +108,9 @@ def load():
     L.lts_simplify_csr.argtypes = [P, I64, P, P, P, I64, P, I64, P, P, P, ctypes.POINTER(lts_report_t),
                                    ctypes.POINTER(lts_options_t), P, ctypes.c_size_t, P]
     L.lts_realize_numeric.argtypes = [P, P, I64, ctypes.c_double, P]
+    L.lts_host_scratch_size.argtypes = [I, P, I64, I64, ctypes.POINTER(ctypes.c_size_t)]
+    L.lts_simplify_host.argtypes = [P, I, P, P, I64, P, I64, P, P, ctypes.POINTER(lts_report_t),
+                                    ctypes.POINTER(lts_options_t), P, ctypes.c_size_t, P, ctypes.c_size_t, P]
     L.lts_extremum_pairs.argtypes = [P, P, I, P, I, ctypes.c_double, P, P, ctypes.POINTER(I64), P,
                                      ctypes.c_size_t, P]
     for name in EXPORTS:

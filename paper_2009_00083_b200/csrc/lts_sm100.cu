@@ -149,7 +149,8 @@ struct DevState {
   int *h_scal = nullptr;  // pinned scalar readback slots
   std::vector<cudaEvent_t> events;
   size_t ev_next = 0;
-  cudaStream_t side = nullptr, side2 = nullptr;
+  cudaStream_t side = nullptr, side2 = nullptr, copys = nullptr;
+  cudaEvent_t g_ready = nullptr, g_copied = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, lfork = nullptr, ljoin = nullptr;
   bool big_attr = false;
   int coop_blocks = 0, coop_per = 0;  // SMs and resident CTAs per SM of k_bv_coop
@@ -355,6 +356,11 @@ struct Ctx {
   bool timing;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
   int64_t flood_launches = 0, flood_slots = 0;
+  // host-buffer call (lts_simplify_host): g goes to the host as soon as a minima pass has
+  // realised it, beside that pass's floods; G at the end
+  float *g_host = nullptr;
+  int32_t *G_host = nullptr;
+  bool g_copy_valid = false, g_copy_pending = false;
   const int *lptr = nullptr, *la = nullptr, *lb = nullptr;  // explicit mesh: link edges (counts only)
 };
 
@@ -1048,8 +1054,23 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
     k_integrate_plain<<<NB(n), 256, 0, s>>>(inv, rev, ni, w.cbits, w.D, new_rank, new_inv);
     g_launches++;
     if (g) {
+      if (c.g_host && c.g_copy_pending) {  // an earlier copy of g still reads it
+        LTS_CUDA(cudaStreamWaitEvent(s, g_cur->g_copied, 0));
+        c.g_copy_pending = false;
+      }
       k_realize<<<NB(C), 256, 0, s>>>(w.skey, w.sval, C, w.rptr, w.verts, g);
       g_launches++;
+      c.g_copy_valid = false;
+      if (c.g_host && kind == 1) {
+        // g is final unless another outer iteration follows: copy it out now,
+        // beside this pass's floods
+        DevState &d = *g_cur;
+        LTS_CUDA(cudaEventRecord(d.g_ready, s));
+        LTS_CUDA(cudaStreamWaitEvent(d.copys, d.g_ready, 0));
+        LTS_CUDA(cudaMemcpyAsync(c.g_host, g, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, d.copys));
+        LTS_CUDA(cudaEventRecord(d.g_copied, d.copys));
+        c.g_copy_valid = c.g_copy_pending = true;
+      }
     }
     if (nbig > 0) {
       // the remaining floods of the large regions; every other localize-phase
@@ -1629,7 +1650,13 @@ static int simplify_impl(Ctx &c, const float *f, const int64_t *pres_max, int64_
     }
   }
   if (it > o.max_iterations) it = o.max_iterations;
-  LTS_CUDA(cudaMemcpyAsync(G, cr, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  if (c.G_host) {
+    LTS_CUDA(cudaMemcpyAsync(c.G_host, cr, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+    if (!c.g_copy_valid) LTS_CUDA(cudaMemcpyAsync(c.g_host, g, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    if (c.g_copy_pending) LTS_CUDA(cudaStreamWaitEvent(s, g_cur->g_copied, 0));
+  } else {
+    LTS_CUDA(cudaMemcpyAsync(G, cr, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  }
   R.ok = ok ? 1 : 0;
   R.outer_iterations = it;
   if (c.timing) {
@@ -1673,6 +1700,65 @@ int lts_simplify(const float *f, int ndim, const int64_t *dims, const int64_t *p
   Ctx c;
   LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
   return simplify_impl(c, f, pres_max, n_max, pres_min, n_min, order, g, G, rep, opt, ws);
+}
+
+// Host-buffer form: the caller's arrays live in (pinned) host memory, as the
+// reference's numpy arrays do.  `dev` is device scratch for f, g and the
+// preserve lists; g leaves for the host while the last pass still floods.
+static size_t host_scratch_layout(int64_t n, int64_t n_max, int64_t n_min, size_t *of, size_t *og, size_t *opm,
+                                  size_t *opn) {
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    off = (off + 255) & ~(size_t)255;
+    const size_t at = off;
+    off += b;
+    return at;
+  };
+  *of = take(sizeof(float) * (size_t)n);
+  *og = take(sizeof(float) * (size_t)n);
+  *opm = take(sizeof(int64_t) * (size_t)std::max<int64_t>(n_max, 1));
+  *opn = take(sizeof(int64_t) * (size_t)std::max<int64_t>(n_min, 1));
+  return off + 256;
+}
+
+int lts_host_scratch_size(int ndim, const int64_t *dims, int64_t n_max, int64_t n_min, size_t *bytes) {
+  if (!dims || !bytes || n_max < 0 || n_min < 0) return lts_set_error(LTS_E_INVALID, "null argument");
+  int64_t n = 1;
+  for (int a = 0; a < ndim; a++) n *= dims[a];
+  size_t a, b, c2, d;
+  *bytes = host_scratch_layout(n, n_max, n_min, &a, &b, &c2, &d);
+  return 0;
+}
+
+int lts_simplify_host(const float *f_host, int ndim, const int64_t *dims, const int64_t *pres_max_host, int64_t n_max,
+                      const int64_t *pres_min_host, int64_t n_min, float *g_host, int32_t *G_host,
+                      lts_report_t *rep, const lts_options_t *opt, void *dev, size_t dev_bytes, void *ws,
+                      size_t ws_bytes, void *stream) {
+  LTS_LOCK;
+  if (!f_host || !g_host || !G_host || !dev) return lts_set_error(LTS_E_INVALID, "null argument");
+  if (n_max < 0 || n_min < 0 || (n_max && !pres_max_host) || (n_min && !pres_min_host))
+    return lts_set_error(LTS_E_INVALID, "bad preserve lists");
+  Ctx c;
+  LTS_TRY(setup(c, ndim, dims, ws, ws_bytes, stream));
+  size_t of, og, opm, opn;
+  if (host_scratch_layout(c.n, n_max, n_min, &of, &og, &opm, &opn) > dev_bytes)
+    return lts_set_error(LTS_E_WORKSPACE, "device scratch too small (lts_host_scratch_size)");
+  char *base = (char *)(((uintptr_t)dev + 255) & ~(uintptr_t)255);
+  float *f_d = (float *)(base + of), *g_d = (float *)(base + og);
+  int64_t *pm_d = (int64_t *)(base + opm), *pn_d = (int64_t *)(base + opn);
+  DevState &d = *g_cur;
+  if (!d.copys) {
+    LTS_CUDA(cudaStreamCreateWithFlags(&d.copys, cudaStreamNonBlocking));
+    LTS_CUDA(cudaEventCreateWithFlags(&d.g_ready, cudaEventDisableTiming));
+    LTS_CUDA(cudaEventCreateWithFlags(&d.g_copied, cudaEventDisableTiming));
+  }
+  cudaStream_t s = c.s;
+  LTS_CUDA(cudaMemcpyAsync(f_d, f_host, sizeof(float) * (size_t)c.n, cudaMemcpyHostToDevice, s));
+  if (n_max) LTS_CUDA(cudaMemcpyAsync(pm_d, pres_max_host, sizeof(int64_t) * (size_t)n_max, cudaMemcpyHostToDevice, s));
+  if (n_min) LTS_CUDA(cudaMemcpyAsync(pn_d, pres_min_host, sizeof(int64_t) * (size_t)n_min, cudaMemcpyHostToDevice, s));
+  c.g_host = g_host;
+  c.G_host = G_host;
+  return simplify_impl(c, f_d, pm_d, n_max, pn_d, n_min, nullptr, g_d, nullptr, rep, opt, ws);
 }
 
 // ---------------------------------------------------------------------------

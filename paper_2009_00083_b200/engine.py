@@ -20,7 +20,7 @@ import torch
 
 from . import _native as N
 from .critical import classify_flags, extrema
-from .errors import ConstraintNotExtremum
+from .errors import ConstraintNotExtremum, FieldError, MeshError
 from .order import OrderField, ScalarField, ZetaPolicy, ZetaMode, compute_order_field, realize_numeric, _as_cuda
 from .triangulation import Triangulation
 
@@ -182,6 +182,55 @@ def simplify_raw(mesh: Triangulation, values: Optional[torch.Tensor], pres_max: 
             rc = N.load().lts_simplify_csr(N.ptr(values), mesh.n, N.ptr(d["indptr"]), N.ptr(d["indices"]), *tail)
     N.check(rc)
     return g, G, rep
+
+
+_host_scratch: dict = {}
+
+
+def simplify_field_host(mesh: Triangulation, f_host: torch.Tensor, constraints: ConstraintSet,
+                        options: Optional[SimplifyOptions] = None, g_out: Optional[torch.Tensor] = None,
+                        G_out: Optional[torch.Tensor] = None, device=None):
+    """simplify_field over HOST buffers (the reference's numpy-facing call,
+    SPEC.md:348-356): f_host float32 (n) in host memory, ideally page-locked;
+    the preserve lists are host id arrays.  Returns (g float32, G int32 ranks,
+    SimplifyReport) as page-locked host tensors (g_out / G_out when given).
+    One C call (lts_simplify_host): the upload, the pass, and the downloads,
+    g leaving for the host while the last pass still floods.  Grids only."""
+    if not mesh.is_grid:
+        raise MeshError("simplify_field_host covers grids; use simplify_field for explicit meshes")
+    N.require_cuda()
+    options = options or SimplifyOptions()
+    if options.zeta is not None:
+        raise ValueError("simplify_field_host realises by contract D1 (zeta=None)")
+    dev = torch.device(device or "cuda")
+    f_host = f_host.reshape(-1)
+    if f_host.device.type != "cpu" or f_host.dtype != torch.float32 or f_host.numel() != mesh.n:
+        raise FieldError("f_host: a host float32 tensor of n values")
+    pm = torch.as_tensor(np.asarray(constraints.preserveMaxima, dtype=np.int64).reshape(-1))
+    pn = torch.as_tensor(np.asarray(constraints.preserveMinima, dtype=np.int64).reshape(-1))
+    g = g_out if g_out is not None else torch.empty(mesh.n, dtype=torch.float32).pin_memory()
+    G = G_out if G_out is not None else torch.empty(mesh.n, dtype=torch.int32).pin_memory()
+    nb = ctypes.c_size_t(0)
+    N.check(N.load().lts_host_scratch_size(mesh.dim, N.dims_arg(mesh.grid_dims), pm.numel(), pn.numel(),
+                                           ctypes.byref(nb)))
+    key = (str(dev), int(nb.value))
+    scratch = _host_scratch.get(key)
+    if scratch is None:
+        _host_scratch.clear()
+        scratch = _host_scratch[key] = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
+    ws = _workspace(mesh, dev)
+    opt = N.lts_options_t()
+    opt.max_iterations = int(options.maxIterations)
+    opt.restore_interior_extrema = 1 if options.restoreInteriorExtrema else 0
+    opt.collect_timing = 1 if options.collectTiming else 0
+    rep = N.lts_report_t()
+    with torch.cuda.device(dev):
+        rc = N.load().lts_simplify_host(N.ptr(f_host), mesh.dim, N.dims_arg(mesh.grid_dims), N.ptr(pm), pm.numel(),
+                                        N.ptr(pn), pn.numel(), N.ptr(g), N.ptr(G), ctypes.byref(rep),
+                                        ctypes.byref(opt), N.ptr(scratch), scratch.numel(), N.ptr(ws), ws.numel(),
+                                        N.stream_ptr(dev))
+    N.check(rc)
+    return g, G, _report(rep)
 
 
 def simplify_field(mesh: Triangulation, f, constraints: ConstraintSet,

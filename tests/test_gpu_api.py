@@ -244,3 +244,35 @@ def test_report_per_region_ni_and_distance_bound(name):
     assert rep.maxNI == max(p.n_iter_max for p in ref.passes)
     assert rep.linf <= bound
     assert rep.linf == float(np.abs(g.values.cpu().numpy().astype(np.float64) - f32.astype(np.float64)).max())
+
+
+def test_simplify_field_host_matches_device_call_and_oracle():
+    """lts_simplify_host: host buffers in, host buffers out (g copied out beside
+    the last pass's floods), same bits as the device-tensor call and the oracle;
+    covers an outer loop > 1 (g copied again) and a pass without regions."""
+    import glob
+    import os
+    gold = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+    picks = [p for p in gold if any(t in p for t in ("quant2d_40", "cfg3_48", "const2d", "crater", "rand3d"))][:6]
+    assert picks
+    for path in picks:
+        z = np.load(path)
+        dims = tuple(int(d) for d in z["dims"])
+        mesh = P.build_grid_triangulation(dims)
+        f_host = torch.from_numpy(np.ascontiguousarray(z["f"], np.float32)).pin_memory()
+        g, G, rep = P.simplify_field_host(mesh, f_host, P.ConstraintSet(preserveMinima=z["pres_min"],
+                                                                        preserveMaxima=z["pres_max"]))
+        assert g.device.type == "cpu" and G.device.type == "cpu"
+        assert rep.ok == bool(z["ok"]) and rep.outerIterations == int(z["outer"])
+        np.testing.assert_array_equal(G.numpy(), z["G_rank"])
+        assert g.numpy().tobytes() == z["g"].tobytes()
+
+
+def test_simplify_field_host_errors():
+    mesh = P.build_grid_triangulation((16, 12))
+    f = torch.rand(16 * 12, dtype=torch.float32)
+    f[5] = float("nan")
+    with pytest.raises(P.FieldError):
+        P.simplify_field_host(mesh, f.pin_memory(), P.ConstraintSet(preserveMinima=[], preserveMaxima=[]))
+    with pytest.raises(P.FieldError):
+        P.simplify_field_host(mesh, torch.rand(7), P.ConstraintSet(preserveMinima=[], preserveMaxima=[]))
