@@ -195,6 +195,7 @@ def other_configs(dev, budget_s: float):
     import torch
 
     import paper_2009_00083_b200 as P
+    from paper_2009_00083_b200 import _native as N
     from paper_2009_00083_b200 import synthetic as S
     hp = os.path.join(ROOT, "tests", "golden", "full_hashes.json")
     digests = json.load(open(hp)) if os.path.exists(hp) else {}
