@@ -423,8 +423,12 @@ __device__ __forceinline__ void lv_jump(const LvArgs &L, int t0, int nt) {
 // beyond the barrier between rounds; the doubling tables are double-buffered.
 constexpr unsigned LV_NIL = 0xffffffffu;
 #ifndef LTS_LV_R4_MAX
-#define LTS_LV_R4_MAX (4 << 20)
+#define LTS_LV_R4_MAX 0x7fffffff
 #endif
+#ifndef LTS_LV_HOPS
+#define LTS_LV_HOPS 3
+#endif
+constexpr int LV_HOPS = LTS_LV_HOPS;  // ancestors visited per round (3: radix-4 doubling, 7: radix-8)
 constexpr int LV_R4_MAX = LTS_LV_R4_MAX;  // active vertices up to which a sweep round jumps four segments
 
 template <int K>
@@ -461,12 +465,13 @@ __device__ __forceinline__ unsigned long long lv_j0(const LvArgs &L, int j, int 
 }
 
 // One doubling round.  FIRST: the pairs are read from the parent pointers (the
-// downward sweep restarts the doubling without an initialisation phase).  R4:
-// the round jumps four segments instead of two (it pushes to / pulls from the
-// ancestors at one, two and three segment lengths), halving the number of
-// rounds, i.e. grid barriers, of the small latency-bound floods.  The round
-// reports whether any vertex still has an ancestor to jump to.
-template <bool UP, bool FIRST, bool R4>
+// downward sweep restarts the doubling without an initialisation phase).  With
+// HOPS = 3 the round jumps four segments instead of two (it pushes to / pulls
+// from the ancestors at one, two and three segment lengths): half the rounds,
+// i.e. half the grid barriers of the small floods and half the passes over
+// the pair arrays of the large ones (cfg4 276 -> 251 ms against HOPS = 1).
+// The round reports whether any vertex still has an ancestor to jump to.
+template <bool UP, bool FIRST, int HOPS>
 __device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned long long *Jc, unsigned long long *Jn,
                                                int *changed, int t0, int nt) {
   int ch = 0;
@@ -485,7 +490,7 @@ __device__ __forceinline__ void lv_sweep_round(const LvArgs &L, const unsigned l
     int hv = UP ? 0 : g[j];
     const int hv0 = hv;
 #pragma unroll
-    for (int hop = 0; hop < (R4 ? 3 : 1); hop++) {
+    for (int hop = 0; hop < HOPS; hop++) {
       if (UP) {
         if (gv >= 0) atomicMax(g + anc, min(min(gv, pmin), (int)anc));
       } else {
@@ -692,7 +697,7 @@ __global__ void __launch_bounds__(256) k_lv_pins(LocArgs A, BigArgs Bg, LvArgs L
 }
 template <bool UP, bool FIRST>
 __global__ void __launch_bounds__(256) k_lv_sweep(LvArgs L, const unsigned long long *Jc, unsigned long long *Jn) {
-  lv_sweep_round<UP, FIRST, false>(L, Jc, Jn, L.ctr + LVC_CHANGED, LV_T0, LV_NT);
+  lv_sweep_round<UP, FIRST, 1>(L, Jc, Jn, L.ctr + LVC_CHANGED, LV_T0, LV_NT);
 }
 __global__ void __launch_bounds__(256) k_lv_classes(LvArgs L) { lv_classes(L, L.ctr + LVC_ACTIVE, LV_T0, LV_NT); }
 __global__ void __launch_bounds__(256) k_lv_sortkeys(LvArgs L) { lv_sortkeys(L, LV_T0, LV_NT); }
@@ -713,6 +718,7 @@ enum { LVK_HOOKS = 0, LVK_CHANGED = 2, LVK_ACTIVE = 5, LVK_INIT = 7, LVK_LEVELS 
 
 // phase clocks of the lead thread (LTS_LEVEL_VERBOSE): chain, prep, scan, hook, jump, beta, classes
 __device__ long long d_lvclk[8];
+__device__ long long d_lvlog[128][4];  // per level (LTS_LEVEL_VERBOSE): active, sweep rounds, sweep cycles, level cycles
 #define LV_TICK(i)                 \
   if (lead) {                      \
     const long long tn = clock64(); \
@@ -771,6 +777,9 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
   while (active > 0) {
     L.level++;
     const int apar = L.level & 1;
+    const long long lv_t0 = clock64();
+    long long lv_ts = 0;
+    int lv_rounds = 0;
     lv_sources(L, plist, np, (int *)Jb, ctr + LVK_NSRC + apar, t0, nt);
     grid.sync();
     lv_prefix<K>(A, Bg, L, (const int *)Jb, *(volatile int *)(ctr + LVK_NSRC + apar), s_front, t0, nt);
@@ -782,21 +791,22 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
       ctr[LVK_NSRC + (apar ^ 1)] = 0;
     }
     grid.sync();
+    lv_ts = clock64();
     for (int sweep = 0; sweep < 2; sweep++) {
       unsigned long long *Jc = Ja, *Jn = Jb;
       for (int it = 0; it < 40; it++) {
+        lv_rounds++;
         cslot = cslot == 2 ? 0 : cslot + 1;
         if (lead) ctr[LVK_CHANGED + (cslot == 2 ? 0 : cslot + 1)] = 0;
         int *chg = ctr + LVK_CHANGED + cslot;
-        // few active vertices: the barriers dominate, jump four segments a round
         if (L.na <= LV_R4_MAX) {
-          if (sweep == 0) lv_sweep_round<true, false, true>(L, Jc, Jn, chg, t0, nt);
-          else if (it == 0) lv_sweep_round<false, true, true>(L, Jc, Jn, chg, t0, nt);
-          else lv_sweep_round<false, false, true>(L, Jc, Jn, chg, t0, nt);
+          if (sweep == 0) lv_sweep_round<true, false, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
+          else if (it == 0) lv_sweep_round<false, true, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
+          else lv_sweep_round<false, false, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
         } else {
-          if (sweep == 0) lv_sweep_round<true, false, false>(L, Jc, Jn, chg, t0, nt);
-          else if (it == 0) lv_sweep_round<false, true, false>(L, Jc, Jn, chg, t0, nt);
-          else lv_sweep_round<false, false, false>(L, Jc, Jn, chg, t0, nt);
+          if (sweep == 0) lv_sweep_round<true, false, 1>(L, Jc, Jn, chg, t0, nt);
+          else if (it == 0) lv_sweep_round<false, true, 1>(L, Jc, Jn, chg, t0, nt);
+          else lv_sweep_round<false, false, 1>(L, Jc, Jn, chg, t0, nt);
         }
         grid.sync();
         unsigned long long *tmp = Jc;
@@ -807,10 +817,17 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
       }
     }
     LV_TICK(5)
+    lv_ts = clock64() - lv_ts;
     int *lnext = bufs[apar];
     lv_classes_list(L, lnext, ctr + LVK_ACTIVE + apar);
     grid.sync();
     LV_TICK(6)
+    if (lead && L.level <= 128) {
+      d_lvlog[L.level - 1][0] = L.na;
+      d_lvlog[L.level - 1][1] = lv_rounds;
+      d_lvlog[L.level - 1][2] = lv_ts;
+      d_lvlog[L.level - 1][3] = clock64() - lv_t0;
+    }
     active = *(volatile int *)(ctr + LVK_ACTIVE + apar);
     plist = L.alist;
     np = L.na;

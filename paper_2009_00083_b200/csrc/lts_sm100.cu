@@ -782,6 +782,13 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
             clk[3] / 1e6, clk[4] / 1e6, clk[5] / 1e6, clk[6] / 1e6);
     memset(clk, 0, sizeof(clk));
     cudaMemcpyToSymbol(d_lvclk, clk, sizeof(clk));
+    if (getenv("LTS_LEVEL_LOG") && levels >= 20) {  // per level: active, sweep rounds, sweep kcycles, level kcycles
+      static long long lg[128][4];
+      cudaMemcpyFromSymbol(lg, d_lvlog, sizeof(lg));
+      for (int i = 0; i < std::min(levels, 128); i++)
+        fprintf(stderr, "[lts]   level %d: active %lld rounds %lld sweep %lld kcyc level %lld kcyc\n", i + 1, lg[i][0],
+                lg[i][1], lg[i][2] / 1000, lg[i][3] / 1000);
+    }
   }
   LTS_KCHECK();
   return 0;
