@@ -280,6 +280,32 @@ def large_field_kernels(dev, hbm):
     return out
 
 
+def grid2d_kernels(dev, hbm):
+    """Order-field sort and classification timed on cfg4's 4096^2 field (the
+    2-D stencil path: six neighbours, tile kernel)."""
+    import torch
+
+    import paper_2009_00083_b200 as P
+    from paper_2009_00083_b200 import _native as N
+    from paper_2009_00083_b200 import synthetic as S
+    C = S.CONFIGS[4]
+    f = torch.from_numpy(S.make_field(4, 0).ravel()).to(dev)
+    mesh = P.build_grid_triangulation(C.dims)
+    ws = N.workspace(mesh.grid_dims, dev)
+    kms = (ctypes.c_double * 4)()
+    N.check(N.load().lts_bench_kernels(N.ptr(f), 2, N.dims_arg(mesh.grid_dims), 10, kms, N.ptr(ws), ws.numel(),
+                                       N.stream_ptr()))
+    n = mesh.n
+    del ws
+    N.release_workspaces()
+    torch.cuda.empty_cache()
+    out = {"config": C.name, "n": n}
+    for key, ms, b in (("order_sort", kms[0], 64), ("classify", kms[1], 5), ("classify_ascent", kms[2], 9)):
+        gbs = b * n / (ms * 1e-3) / 1e9
+        out[key] = {"ms": ms, "bytes_per_voxel": b, "achieved_gbs": gbs, "frac": gbs / hbm}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -457,9 +483,10 @@ def main():
     # cfg5 (512^3): the same eight waves as synthetic.cfg5 (numpy draws), the
     # N(0, 0.02) noise drawn on the device (torch generator) so the field is
     # built in well under a second; kernels as above (rank 0, N = 1).
-    kernels_large = None
+    kernels_large = kernels_2d = None
     if rank == 0 and world == 1 and not args.no_large:
         kernels_large = large_field_kernels(dev, hbm)
+        kernels_2d = grid2d_kernels(dev, hbm)
 
     # ---- other BASELINE configs (rank 0, N = 1) -------------------------------
     configs = None
@@ -485,7 +512,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(cfg, args, n, (pm.size, pn.size), world),
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
-            "kernels_large": kernels_large,
+            "kernels_large": kernels_large, "kernels_2d": kernels_2d,
             "phases_ms": phases, "cpu_baseline": cpu, "clocks": clk.summary(), "configs": configs,
             "report": {"ok": report.ok, "outer": report.outerIterations,
                        "passes": [p.__dict__ for p in report.passes]},

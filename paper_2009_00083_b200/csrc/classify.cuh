@@ -323,11 +323,15 @@ __global__ void __launch_bounds__(CP_TX *CP_TY) k_classify_tile(Grid g, const in
 
 inline bool launch_classify_zreg(const Grid &g, const int32_t *rank, uint8_t *flags, int32_t *ptr, int ptr_kind,
                                  cudaStream_t s);
+// 2-D strip kernel (classify_2d.cuh); false = not applicable
+inline bool launch_classify_2d(const Grid &g, const int32_t *rank, uint8_t *flags, int32_t *ptr, int ptr_kind,
+                               cudaStream_t s);
 
 inline void launch_classify(const Grid &g, const int32_t *rank, uint8_t *flags, int16_t *lower,
                             int16_t *upper, const uint8_t *lut, int32_t *ptr, int ptr_kind,
                             cudaStream_t s) {
   if (lower == nullptr && launch_classify_zreg(g, rank, flags, ptr, ptr_kind, s)) return;
+  if (lower == nullptr && launch_classify_2d(g, rank, flags, ptr, ptr_kind, s)) return;
   dim3 blk(CP_TX, CP_TY);
   dim3 grd((g.nx + CP_W - 1) / CP_W, (g.ny + CP_TY * CP_RY - 1) / (CP_TY * CP_RY),
            g.ndim == 2 ? 1 : (g.nz + CP_ZC - 1) / CP_ZC);

@@ -23,6 +23,7 @@
 #include "sort.cuh"
 #include "classify.cuh"
 #include "classify_zreg.cuh"
+#include "classify_2d.cuh"
 #include "discover.cuh"
 #include "localize.cuh"
 #include "localize_big.cuh"
