@@ -257,3 +257,21 @@ def test_level_floods_capped_regions_golden(path, monkeypatch):
     assert rep.ok == bool(z["ok"]) and rep.outerIterations == int(z["outer"])
     np.testing.assert_array_equal(G.rank32.cpu().numpy(), z["G_rank"])
     assert g.values.cpu().numpy().tobytes() == z["g"].tobytes()
+
+
+def test_classify_2d_strip_kernel_matches_oracle():
+    """2-D grids of a million pixels take the strip kernel (classify_2d.cuh):
+    flags against the oracle's extrema, and the pointer variants through a
+    full pass (ascent / descent forests feed discover)."""
+    f = S.cfg1(3, N=1024)
+    dims, f32, pm, pn, ref = _oracle_case(np.asarray(f, np.float32), 16, 1)
+    mesh = _mesh(dims)
+    F = P.compute_order_field(P.ScalarField(mesh, _cu(f32)))
+    mn, mx = P.extrema(mesh, F)
+    omn, omx = O.extrema(dims, F.rank32.cpu().numpy())
+    np.testing.assert_array_equal(np.sort(mn.cpu().numpy()), omn)
+    np.testing.assert_array_equal(np.sort(mx.cpu().numpy()), omx)
+    g, G, rep = P.simplify_field(mesh, _cu(f32), P.ConstraintSet(preserveMinima=pn, preserveMaxima=pm))
+    assert rep.ok == ref.ok and rep.outerIterations == ref.outer_iterations
+    np.testing.assert_array_equal(G.rank32.cpu().numpy(), ref.G_rank)
+    assert g.values.cpu().numpy().tobytes() == ref.g.tobytes()
