@@ -431,14 +431,21 @@ constexpr unsigned LV_NIL = 0xffffffffu;
 constexpr int LV_HOPS = LTS_LV_HOPS;  // ancestors visited per round (3: radix-4 doubling, 7: radix-8)
 constexpr int LV_R4_MAX = LTS_LV_R4_MAX;  // active vertices up to which a sweep round jumps four segments
 
-template <int K>
+// MARKS: the flood prefix (lv_prefix) has pushed every member neighbour of a
+// task's source set into its frontier and marked it: the pins are the marked
+// vertices that stayed unplaced, no neighbour row is read.  Without the prefix
+// (host-driven path: plain ascent chains) every member scans its neighbours.
+template <int K, bool MARKS>
 __device__ __forceinline__ void lv_pins(const LocArgs &A, const BigArgs &Bg, const LvArgs &L, unsigned long long *J,
                                         int t0, int nt) {
+  const int mark = -(3 + L.level);
   LV_ACT(j, L) {
     const int tk = L.task[j];
     if (tk < 0) continue;
     bool pin = L.sval[j] == tk;  // a source of an ascending flood (virtual root)
-    if (!pin) {
+    if (MARKS) {
+      pin = pin || L.lvl[j] == mark;
+    } else if (!pin) {
       const LvRef R = lv_ref(A, Bg, j);
       int q[K];
       lv_load_row<K>(Bg, R, j, q);
@@ -693,7 +700,7 @@ __global__ void __launch_bounds__(256) k_lv_hook(LvArgs L) { lv_hook(L, L.ctr + 
 __global__ void __launch_bounds__(256) k_lv_jump(LvArgs L) { lv_jump(L, LV_T0, LV_NT); }
 template <int K>
 __global__ void __launch_bounds__(256) k_lv_pins(LocArgs A, BigArgs Bg, LvArgs L, unsigned long long *J) {
-  lv_pins<K>(A, Bg, L, J, LV_T0, LV_NT);
+  lv_pins<K, false>(A, Bg, L, J, LV_T0, LV_NT);
 }
 template <bool UP, bool FIRST>
 __global__ void __launch_bounds__(256) k_lv_sweep(LvArgs L, const unsigned long long *Jc, unsigned long long *Jn) {
@@ -785,7 +792,7 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
     lv_prefix<K>(A, Bg, L, (const int *)Jb, *(volatile int *)(ctr + LVK_NSRC + apar), s_front, t0, nt);
     grid.sync();
     LV_TICK(0)
-    lv_pins<K>(A, Bg, L, Ja, t0, nt);
+    lv_pins<K, true>(A, Bg, L, Ja, t0, nt);
     if (lead) {
       ctr[LVK_ACTIVE + apar] = 0;
       ctr[LVK_NSRC + (apar ^ 1)] = 0;
