@@ -155,6 +155,7 @@ struct DevState {
   cudaEvent_t fork = nullptr, join = nullptr, lfork = nullptr, ljoin = nullptr;
   bool big_attr = false;
   int coop_blocks = 0, coop_per = 0;  // SMs and resident CTAs per SM of k_bv_coop
+  int coop_ok = -1;  // cudaDevAttrCooperativeLaunch
   int lv_blocks[4] = {0, 0, 0, 0}, lv_per[4] = {0, 0, 0, 0};  // cooperative grid of the level floods, per ndim
 };
 static DevState g_dev[LTS_MAX_DEV];
@@ -657,7 +658,18 @@ static int big_level_flood(Ctx &c, const LocArgs &A, const BigArgs &B) {
   int *hc = c.h_scal + SC_LV;
   int levels = 0, rounds_total = 0, lv_grid = 1;
   LTS_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(int) * LVC_N, s));
-  const bool host_loop = getenv("LTS_LEVEL_HOST") != nullptr;  // debugging: one launch per phase
+  bool host_loop = getenv("LTS_LEVEL_HOST") != nullptr;  // debugging: one launch per phase
+  {
+    // devices without cooperative launches take the host-driven loop as well
+    DevState &d = *g_cur;
+    if (d.coop_ok < 0) {
+      int dev = 0, ok = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+      d.coop_ok = ok ? 1 : 0;
+    }
+    if (!d.coop_ok) host_loop = true;
+  }
   const int nd = c.g.ndim;
   if (!host_loop) {
     // every level in one cooperative launch
