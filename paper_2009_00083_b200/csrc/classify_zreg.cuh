@@ -41,7 +41,7 @@ constexpr int CZ_PLANE = CZ_BX * CZ_BY;
 constexpr int CZ_SLOT = (CZ_PLANE * 4 + 127) / 128 * 32;    // 128-byte aligned destinations
 constexpr int CZ_RING = 6;
 #ifndef LTS_CZ_MINB
-#define LTS_CZ_MINB 3
+#define LTS_CZ_MINB 4
 #endif
 
 // the 16 stencil cells of a 4-voxel strip in one plane: row y-1 at x-1..x+3,
