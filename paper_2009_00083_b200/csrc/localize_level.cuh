@@ -15,20 +15,29 @@
 // i.e. the source of the flood task in which v is a record low) with children
 // visited in decreasing key, and the subtree sizes of F are the class sizes.
 // Bottleneck paths are paths of a maximum spanning tree under the edge weight
-// min(key u, key v), so one level is data-parallel over all tasks of all
-// regions at once:
-//   1. Boruvka maximum spanning forest of every task's member graph, kept
-//      rooted at the task's source (a hooking component reverses the path from
-//      its hook vertex to its old root); the source's component never hooks;
-//   2. beta by pointer jumping (argmin of the key along the root path);
-//   3. class sizes, new tasks (source beta(v)) for the vertices off the trunk.
-// Levels repeat until every vertex is a trunk vertex of some level; a final
-// stable sort by F-parent, a segmented prefix of the class sizes and pointer
-// jumping over F give every vertex its extraction index.  Ascending floods
-// (many sources, min-first) are the same flood on reversed keys from a virtual
-// root adjacent to every source.  The decomposition was checked against heap
-// floods of the reference on the regions of the BASELINE configs (2-D and 3-D,
-// single and multi source) and is covered bit-exactly by the parity tests.
+// min(key u, key v), so the flood of all flagged regions is data-parallel, one
+// cooperative kernel (k_lv_coop) with grid barriers between its phases:
+//   1. once per flood, the Boruvka maximum spanning forest R of the region
+//      graphs, kept rooted at each region's source (a hooking component
+//      reverses the path from its hook vertex to its old root; the source's
+//      component never hooks);
+//   2. levels: R is never re-rooted.  A class is a connected piece of R and the
+//      spanning forest of a later task lies inside R's edges plus the edges
+//      from the task's source set to the class, so beta of a level is a
+//      multi-source bottleneck on R restricted to the class (lv_pins, two
+//      pointer-doubling sweeps); trunk vertices are placed, the others move to
+//      the task of their class's trunk vertex (lv_classes_list);
+//   3. before the sweeps every task places a prefix of its exact order with a
+//      one-warp flood (lv_prefix), so a climb through a bumpy field crosses
+//      many bumps per level.
+// Levels repeat until every vertex is placed; a final stable sort by F-parent, a
+// segmented prefix of the class sizes and pointer jumping over F give every
+// vertex its extraction index.  Ascending floods (many sources, min-first) are
+// the same flood on reversed keys from a virtual root adjacent to every
+// source.  The decomposition was checked against heap floods of the reference
+// on the regions of the BASELINE configs (2-D and 3-D, single and multi
+// source) and is covered bit-exactly by the parity tests (both flood paths
+// forced in turn, randomised sweeps, the full-size digests).
 //
 // Everything is indexed in "key space": j = jb(region) + key, keys in [0, k],
 // jb = bpre[qi] + qi; within a region j is monotone in the key, so keys are
@@ -422,14 +431,10 @@ __device__ __forceinline__ void lv_jump(const LvArgs &L, int t0, int nt) {
 // max / min are idempotent, so the in-place updates of g need no ordering
 // beyond the barrier between rounds; the doubling tables are double-buffered.
 constexpr unsigned LV_NIL = 0xffffffffu;
-#ifndef LTS_LV_R4_MAX
-#define LTS_LV_R4_MAX 0x7fffffff
-#endif
 #ifndef LTS_LV_HOPS
 #define LTS_LV_HOPS 3
 #endif
 constexpr int LV_HOPS = LTS_LV_HOPS;  // ancestors visited per round (3: radix-4 doubling, 7: radix-8)
-constexpr int LV_R4_MAX = LTS_LV_R4_MAX;  // active vertices up to which a sweep round jumps four segments
 
 // MARKS: the flood prefix (lv_prefix) has pushed every member neighbour of a
 // task's source set into its frontier and marked it: the pins are the marked
@@ -806,15 +811,9 @@ __global__ void __launch_bounds__(32 * LV_WARPS) k_lv_coop(LocArgs A, BigArgs Bg
         cslot = cslot == 2 ? 0 : cslot + 1;
         if (lead) ctr[LVK_CHANGED + (cslot == 2 ? 0 : cslot + 1)] = 0;
         int *chg = ctr + LVK_CHANGED + cslot;
-        if (L.na <= LV_R4_MAX) {
-          if (sweep == 0) lv_sweep_round<true, false, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
-          else if (it == 0) lv_sweep_round<false, true, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
-          else lv_sweep_round<false, false, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
-        } else {
-          if (sweep == 0) lv_sweep_round<true, false, 1>(L, Jc, Jn, chg, t0, nt);
-          else if (it == 0) lv_sweep_round<false, true, 1>(L, Jc, Jn, chg, t0, nt);
-          else lv_sweep_round<false, false, 1>(L, Jc, Jn, chg, t0, nt);
-        }
+        if (sweep == 0) lv_sweep_round<true, false, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
+        else if (it == 0) lv_sweep_round<false, true, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
+        else lv_sweep_round<false, false, LV_HOPS>(L, Jc, Jn, chg, t0, nt);
         grid.sync();
         unsigned long long *tmp = Jc;
         Jc = Jn;
