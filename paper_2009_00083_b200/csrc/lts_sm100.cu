@@ -911,7 +911,7 @@ static int run_pass(Ctx &c, int kind, const int *rank, const int *inv, const uin
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&coop_per, k_bv_coop, 256, 0);
         coop_per = std::max(1, coop_per);
       }
-      const int coop_blocks = coop_sm * std::min(coop_per, nm >= (1 << 18) ? 4 : LTS_BV_COOP_PER_SM);
+      const int coop_blocks = coop_sm * std::min(coop_per, nm >= (1 << 16) ? 4 : LTS_BV_COOP_PER_SM);
       BvArgs ba{w.mlist, nm, w.comp, w.par, w.wc, w.rt, w.acc, w.scal + SC_ERR, w.cst, w.vcls, w.bestP, w.best,
                 ea, eb, ew, w.scal + SC_ECOUNT, w.scal + SC_BVSTATE};
       void *kargs[] = {&ba};
