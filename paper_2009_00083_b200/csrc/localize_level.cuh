@@ -657,11 +657,19 @@ __device__ __forceinline__ void lv_pos_round(const LvArgs &L, int *changed, int 
   int ch = 0;
   LV_FOR(j, L) {
     if (L.fp[j] == LV_NONE) continue;
-    const unsigned long long a = L.pm[j];
-    const unsigned anc = (unsigned)(a & 0xffffffffu);
+    unsigned long long a = L.pm[j];
+    unsigned acc = (unsigned)(a >> 32), anc = (unsigned)(a & 0xffffffffu);
     if (L.fp[anc] == LV_NONE) continue;
-    const unsigned long long b = L.pm[anc];
-    L.pm[j] = lv_pack((unsigned)(a >> 32) + (unsigned)(b >> 32), (unsigned)(b & 0xffffffffu));
+    // up to three jumps per round: every pair read is a consistent (offset,
+    // ancestor) snapshot, so any number of hops keeps the invariant
+#pragma unroll
+    for (int hop = 0; hop < 3; hop++) {
+      const unsigned long long b = L.pm[anc];
+      acc += (unsigned)(b >> 32);
+      anc = (unsigned)(b & 0xffffffffu);
+      if (L.fp[anc] == LV_NONE) break;
+    }
+    L.pm[j] = lv_pack(acc, anc);
     ch = 1;
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
