@@ -54,7 +54,9 @@ __global__ void k_integrate_plain(const int *__restrict__ inv, int rev, int n,
   }
 }
 
-// sorted sibling groups: sib_rid sorted by saddle rank (stable), pos_of[rid]
+// sorted sibling groups: sib_rid sorted by saddle rank (stable), pos_of[rid].
+// Every region sharing a saddle holds one of the saddle's neighbours, so a
+// group has at most K members (14 on grids, 16 on meshes): the loop is O(K).
 __device__ __forceinline__ int sib_offset(int l, int rid, int top_r, const int *rsad,
                                           const int *rsize, const int *rtop, const int *sib_rid,
                                           const int *pos_of, int R) {
